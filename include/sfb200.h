@@ -1,0 +1,146 @@
+/*
+ * sfb200.h — C-ABI of libsfb200.so, the sm_100a execution backend behind the
+ * stageflow-compatible front-end in paper_1903_01855_b200/.
+ *
+ * Every entry point is extern "C", takes plain pointers and sizes, returns an
+ * int status (SF_OK == 0) and leaves a message for sf_last_error() on
+ * failure.  All device work is stream-ordered on the device's single compute
+ * stream; host-visible results (sf_memcpy_d2h) synchronise that stream.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src):
+ *   sf_alloc / sf_free / sf_memcpy_*  -> numpy buffer ownership in
+ *        stageflow/tensor.py:38-70 (Tensor storage), :138-172 (host interchange)
+ *        and the relabelling copies of stageflow/ops.py:245-286
+ *   sf_elementwise  -> _binary_kernel / _unary_kernel / _greater_kernel /
+ *        _broadcast_to_kernel / _identity_kernel, stageflow/kernels.py:116-181,
+ *        :222-232, :263-279, :307-315
+ *   sf_reduce       -> _reduce_kernel (np.sum / np.mean), stageflow/kernels.py:323-364
+ *   sf_matmul       -> _matmul_kernel (np.matmul), stageflow/kernels.py:184-208
+ *   sf_transpose2d  -> _transpose_kernel, stageflow/kernels.py:211-219
+ *   sf_fill / sf_eye-> _eye_kernel / gradients.zeros_for/ones_for,
+ *        stageflow/kernels.py:282-292, stageflow/gradients.py:65-76
+ *   sf_rng          -> _random_normal_kernel (Runtime.draw), stageflow/kernels.py:372-384
+ *   sf_dropout      -> _dropout_kernel, stageflow/kernels.py:387-404
+ *   sf_jit_* / sf_plan_* -> execute_graph + _Plan, stageflow/executor.py:58-269
+ *        (the traced graph is lowered once into fused kernels and replayed)
+ */
+#ifndef SFB200_H_
+#define SFB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SF_OK 0
+#define SF_ERR_INVALID 1
+#define SF_ERR_CUDA 2
+#define SF_ERR_OOM 3
+#define SF_ERR_NVRTC 4
+#define SF_ERR_UNSUPPORTED 5
+#define SF_ERR_NO_DEVICE 6
+
+/* dtype tags (same values as the reference wire tags, stageflow/dtypes.py:63-69) */
+#define SF_DTYPE_F32 1
+#define SF_DTYPE_F64 2
+#define SF_DTYPE_I32 3
+#define SF_DTYPE_BOOL 4
+
+#define SF_MAX_DIMS 8
+
+/* ---------------------------------------------------------------- runtime */
+const char* sf_last_error(void);
+int sf_version(void);
+/* Enumerate CUDA devices; creates one non-blocking stream and one caching
+ * allocator per device.  Idempotent. */
+int sf_init(int* n_devices);
+int sf_device_info(int dev, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
+/* Route all work for `dev` onto an external stream (e.g. torch's current
+ * stream, for NCCL interop); NULL restores the backend's own stream. */
+int sf_set_stream(int dev, void* stream);
+int sf_get_stream(int dev, void** stream);
+int sf_device_sync(int dev);
+
+int sf_alloc(int dev, size_t bytes, void** p);
+int sf_free(int dev, void* p);
+int sf_mem_stats(int dev, size_t* bytes_in_use, size_t* bytes_cached);
+int sf_trim(int dev);
+
+/* host <-> device copies.  h2d copies the host bytes before returning (the
+ * caller may reuse `src` immediately); d2h blocks until the data is on the
+ * host. */
+int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes);
+int sf_memcpy_d2h(int dev, void* dst, const void* src, size_t bytes);
+int sf_memcpy_d2d(int dev, void* dst, const void* src, size_t bytes);
+int sf_memcpy_p2p(int dst_dev, void* dst, int src_dev, const void* src, size_t bytes);
+
+/* ------------------------------------------------------- eager primitives
+ * Each launch allocates its output(s) from the caching allocator when the
+ * passed *out is NULL, otherwise writes into *out. */
+
+/* Packed elementwise descriptor (little-endian, natural alignment). */
+typedef struct sf_ew_desc {
+  int32_t op;          /* SF_OP_* from csrc/sf_ops.cuh */
+  int32_t dtype;       /* input dtype; the output dtype follows the op */
+  int32_t ndim;        /* <= SF_MAX_DIMS, 0 for scalars */
+  int32_t n_in;        /* 1, 2 or 3 */
+  const void* in[3];   /* NULL => operand is the immediate imm[i] */
+  double imm[3];
+  int64_t shape[SF_MAX_DIMS];       /* output shape */
+  int64_t strides[3][SF_MAX_DIMS];  /* element strides per operand, 0 = broadcast */
+} sf_ew_desc;
+
+int sf_elementwise(int dev, const sf_ew_desc* desc, void** out);
+/* op: 0 = sum, 1 = mean.  axes_mask bit i set => axis i reduced. */
+int sf_reduce(int dev, int op, int dtype, int ndim, const int64_t* shape, uint32_t axes_mask,
+              const void* in, void** out);
+/* C[m,n] = op(A) @ op(B), row-major; trans_* = 1 reads the operand transposed. */
+int sf_matmul(int dev, int dtype, int64_t m, int64_t n, int64_t k, const void* a, int trans_a,
+              const void* b, int trans_b, void** out);
+int sf_transpose2d(int dev, int dtype, int64_t rows, int64_t cols, const void* in, void** out);
+int sf_fill(int dev, int dtype, int64_t n, double value, void** out);
+int sf_eye(int dev, int dtype, int64_t n, void** out);
+int sf_cast(int dev, int src_dtype, int dst_dtype, int64_t n, const void* in, void** out);
+/* Device Philox RNG.  kind: 0 = standard normal, 1 = uniform [0,1).
+ * offset == UINT64_MAX reserves the next n counters from the device stream. */
+int sf_rng_seed(int dev, uint64_t seed);
+int sf_rng_reserve(int dev, uint64_t n, uint64_t* offset);
+int sf_rng(int dev, int kind, int dtype, int64_t n, uint64_t offset, void** out);
+/* dropout: mask = (u >= rate) / (1 - rate) in dtype; out = x * mask.  u is a
+ * buffer of uniforms of dtype u_dtype (host-drawn parity mode) or NULL to
+ * draw from the device Philox stream. */
+int sf_dropout(int dev, int dtype, int64_t n, const void* x, const void* u, int u_dtype,
+               double rate, void** out, void** mask);
+
+/* ------------------------------------------------------- staged graphs */
+/* Compile CUDA C++ source (which may #include "sf_ops.cuh") for sm_100a with
+ * NVRTC and load it; returns an opaque kernel handle. Cached by source. */
+int sf_jit_compile(const char* kernel_name, const char* source, void** kernel);
+const char* sf_jit_log(void);
+/* Launch a jitted kernel with one by-value parameter blob. */
+int sf_jit_launch(int dev, void* kernel, unsigned grid, unsigned block, unsigned smem,
+                  const void* params, size_t params_bytes);
+
+/* A plan is a lowered graph function: a list of steps over value slots
+ * (inputs, plan-owned constants, per-call temporaries, outputs).  The binary
+ * plan format is documented in csrc/sf_plan.cpp. */
+int sf_plan_create(int dev, const void* desc, size_t desc_bytes, void** plan);
+/* Runs the plan on its device's stream.  inputs: n_inputs device pointers;
+ * outputs: receives n_outputs freshly allocated device pointers (ownership
+ * passes to the caller, release with sf_free). */
+int sf_plan_run(void* plan, const void* const* inputs, void** outputs);
+int sf_plan_info(void* plan, int* n_inputs, int* n_outputs, int* n_steps, int* n_launches);
+int sf_plan_destroy(void* plan);
+
+/* ------------------------------------------------------- counters */
+/* number of kernels this library has launched on `dev` since sf_init */
+int sf_launch_count(int dev, uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFB200_H_ */

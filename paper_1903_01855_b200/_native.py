@@ -1,0 +1,446 @@
+"""ctypes binding of libsfb200.so (the C-ABI declared in include/sfb200.h).
+
+This is the only module that talks to the native library.  Every call
+checks the returned status and raises: ``DeviceUnavailable`` when no GPU or
+no built library is present, ``KernelError`` for any other native failure.
+There is no host fallback anywhere behind these functions.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+import threading
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from .errors import DeviceUnavailable, KernelError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsfb200.so")
+
+# ---- opcodes: must match csrc/sf_ops.cuh ------------------------------------
+OP = dict(
+    identity=0, neg=1, exp=2, log=3, softplus=4, relu=5, step_positive=6, tanh=7,
+    sqrt=8, rsqrt=9, sigmoid=10, abs=11, square=12, isfinite=13, logical_not=14,
+    reciprocal=15, cos=16, sin=17,
+    add=32, sub=33, mul=34, div=35, greater=36, maximum=37, minimum=38, less=39,
+    equal=40, greater_equal=41,
+    select=64,
+)
+BOOL_RESULT_OPS = frozenset(("greater", "less", "equal", "greater_equal", "isfinite",
+                             "logical_not"))
+
+SF_OK, SF_ERR_NO_DEVICE = 0, 6
+MAX_DIMS = 8
+
+_lib: Optional[ctypes.CDLL] = None
+_lib_lock = threading.Lock()
+_load_error: Optional[str] = None
+_tls = threading.local()
+
+_VP = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_PVP = ctypes.POINTER(ctypes.c_void_p)
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    sig = {
+        "sf_last_error": (ctypes.c_char_p, []),
+        "sf_version": (ctypes.c_int, []),
+        "sf_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+        "sf_device_info": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_size_t)]),
+        "sf_set_stream": (ctypes.c_int, [ctypes.c_int, _VP]),
+        "sf_get_stream": (ctypes.c_int, [ctypes.c_int, _PVP]),
+        "sf_device_sync": (ctypes.c_int, [ctypes.c_int]),
+        "sf_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_size_t, _PVP]),
+        "sf_free": (ctypes.c_int, [ctypes.c_int, _VP]),
+        "sf_mem_stats": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
+                                         ctypes.POINTER(ctypes.c_size_t)]),
+        "sf_trim": (ctypes.c_int, [ctypes.c_int]),
+        "sf_memcpy_h2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
+        "sf_memcpy_d2h": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
+        "sf_memcpy_d2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
+        "sf_memcpy_p2p": (ctypes.c_int, [ctypes.c_int, _VP, ctypes.c_int, _VP, ctypes.c_size_t]),
+        "sf_elementwise": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _PVP]),
+        "sf_reduce": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_char_p, ctypes.c_uint32, _VP, _PVP]),
+        "sf_matmul": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _I64, _I64, _VP,
+                                      ctypes.c_int, _VP, ctypes.c_int, _PVP]),
+        "sf_transpose2d": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _I64, _VP, _PVP]),
+        "sf_fill": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, ctypes.c_double, _PVP]),
+        "sf_eye": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _PVP]),
+        "sf_cast": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _VP, _PVP]),
+        "sf_rng_seed": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64]),
+        "sf_rng_reserve": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64,
+                                           ctypes.POINTER(ctypes.c_uint64)]),
+        "sf_rng": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64,
+                                   ctypes.c_uint64, _PVP]),
+        "sf_dropout": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _VP, _VP, ctypes.c_int,
+                                       ctypes.c_double, _PVP, _PVP]),
+        "sf_jit_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _PVP]),
+        "sf_jit_log": (ctypes.c_char_p, []),
+        "sf_jit_launch": (ctypes.c_int, [ctypes.c_int, _VP, ctypes.c_uint, ctypes.c_uint,
+                                          ctypes.c_uint, ctypes.c_char_p, ctypes.c_size_t]),
+        "sf_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t, _PVP]),
+        "sf_plan_run": (ctypes.c_int, [_VP, _VP, _VP]),
+        "sf_plan_info": (ctypes.c_int, [_VP] + [ctypes.POINTER(ctypes.c_int)] * 4),
+        "sf_plan_destroy": (ctypes.c_int, [_VP]),
+        "sf_launch_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+EXPORTED_SYMBOLS = (
+    "sf_last_error", "sf_version", "sf_init", "sf_device_info", "sf_set_stream",
+    "sf_get_stream", "sf_device_sync", "sf_alloc", "sf_free", "sf_mem_stats", "sf_trim",
+    "sf_memcpy_h2d", "sf_memcpy_d2h", "sf_memcpy_d2d", "sf_memcpy_p2p", "sf_elementwise",
+    "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
+    "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
+    "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
+)
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libsfb200.so (no device needed for the load itself)."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                _load_error = (f"native library {LIB_PATH} is not built; run "
+                               "`python -c 'import __graft_entry__ as g; g.build()'`")
+                raise DeviceUnavailable(_load_error)
+            lib = ctypes.CDLL(LIB_PATH)
+            _declare(lib)
+            _lib = lib
+    return _lib
+
+
+def _err(lib, rc: int, what: str):
+    msg = (lib.sf_last_error() or b"").decode(errors="replace")
+    if rc == SF_ERR_NO_DEVICE:
+        return DeviceUnavailable(f"{what}: {msg}")
+    return KernelError(f"{what}: {msg}")
+
+
+def lib() -> ctypes.CDLL:
+    return load_library()
+
+
+_device_count: Optional[int] = None
+
+
+def device_count() -> int:
+    """Number of usable CUDA devices; 0 if the library or GPU is missing."""
+    global _device_count
+    if _device_count is None:
+        try:
+            L = load_library()
+        except (DeviceUnavailable, OSError):
+            _device_count = 0
+            return 0
+        n = ctypes.c_int(0)
+        _device_count = n.value if L.sf_init(ctypes.byref(n)) == SF_OK else 0
+    return _device_count
+
+
+def require_device():
+    if device_count() == 0:
+        L = None
+        try:
+            L = load_library()
+        except DeviceUnavailable:
+            raise
+        n = ctypes.c_int(0)
+        rc = L.sf_init(ctypes.byref(n))
+        raise _err(L, rc if rc else SF_ERR_NO_DEVICE, "GPU backend unavailable")
+    return lib()
+
+
+def _outslot():
+    p = getattr(_tls, "out", None)
+    if p is None:
+        p = _tls.out = ctypes.c_void_p(0)
+        _tls.outref = ctypes.byref(p)
+        _tls.out2 = ctypes.c_void_p(0)
+        _tls.out2ref = ctypes.byref(_tls.out2)
+    p.value = None
+    return p, _tls.outref
+
+
+# ---------------------------------------------------------------- buffers
+class DeviceBuffer:
+    """Owns one allocation from the device's caching allocator."""
+
+    __slots__ = ("dev", "ptr", "nbytes", "__weakref__")
+
+    def __init__(self, dev: int, ptr: int, nbytes: int):
+        self.dev = dev
+        self.ptr = ptr
+        self.nbytes = nbytes
+
+    def __del__(self):
+        ptr = self.ptr
+        if ptr:
+            self.ptr = 0
+            try:
+                _lib.sf_free(self.dev, ptr)
+            except Exception:  # interpreter shutdown
+                pass
+
+
+def alloc(dev: int, nbytes: int) -> DeviceBuffer:
+    L = require_device()
+    out, ref = _outslot()
+    rc = L.sf_alloc(dev, max(1, nbytes), ref)
+    if rc:
+        raise _err(L, rc, "sf_alloc")
+    return DeviceBuffer(dev, out.value, nbytes)
+
+
+def upload(dev: int, arr: np.ndarray) -> DeviceBuffer:
+    arr = np.ascontiguousarray(arr)
+    buf = alloc(dev, arr.nbytes)
+    if arr.nbytes:
+        rc = _lib.sf_memcpy_h2d(dev, buf.ptr, arr.ctypes.data, arr.nbytes)
+        if rc:
+            raise _err(_lib, rc, "sf_memcpy_h2d")
+    return buf
+
+
+def download(buf: DeviceBuffer, np_dtype, shape) -> np.ndarray:
+    out = np.empty(shape, dtype=np_dtype)
+    if out.nbytes:
+        rc = _lib.sf_memcpy_d2h(buf.dev, out.ctypes.data, buf.ptr, out.nbytes)
+        if rc:
+            raise _err(_lib, rc, "sf_memcpy_d2h")
+    return out
+
+
+def copy_d2d(dev: int, dst: int, src: int, nbytes: int) -> None:
+    rc = _lib.sf_memcpy_d2d(dev, dst, src, nbytes)
+    if rc:
+        raise _err(_lib, rc, "sf_memcpy_d2d")
+
+
+def copy_p2p(dst_dev: int, dst: int, src_dev: int, src: int, nbytes: int) -> None:
+    rc = _lib.sf_memcpy_p2p(dst_dev, dst, src_dev, src, nbytes)
+    if rc:
+        raise _err(_lib, rc, "sf_memcpy_p2p")
+
+
+def sync(dev: int) -> None:
+    L = require_device()
+    rc = L.sf_device_sync(dev)
+    if rc:
+        raise _err(L, rc, "sf_device_sync")
+
+
+def stream_of(dev: int) -> int:
+    L = require_device()
+    p = ctypes.c_void_p(0)
+    rc = L.sf_get_stream(dev, ctypes.byref(p))
+    if rc:
+        raise _err(L, rc, "sf_get_stream")
+    return p.value or 0
+
+
+def set_stream(dev: int, stream: int) -> None:
+    L = require_device()
+    rc = L.sf_set_stream(dev, stream or None)
+    if rc:
+        raise _err(L, rc, "sf_set_stream")
+
+
+def mem_stats(dev: int):
+    L = require_device()
+    a, b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    L.sf_mem_stats(dev, ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
+
+
+def launch_count(dev: int) -> int:
+    L = load_library()
+    c = ctypes.c_uint64(0)
+    L.sf_launch_count(dev, ctypes.byref(c))
+    return c.value
+
+
+def rng_seed(dev: int, seed: int) -> None:
+    rc = lib().sf_rng_seed(dev, seed & 0xFFFFFFFFFFFFFFFF)
+    if rc:
+        raise _err(_lib, rc, "sf_rng_seed")
+
+
+# ---------------------------------------------------------------- launches
+# sf_ew_desc header: op, dtype, ndim, n_in, in[3], imm[3]; the geometry
+# (shape[8], strides[3][8]) is packed once per shape signature by the caller.
+EW_HEAD = struct.Struct("<iiii3Q3d")
+EW_GEOM = struct.Struct("<8q24q")
+
+
+def pack_geometry(out_shape: Sequence[int], strides: Sequence[Sequence[int]]) -> bytes:
+    nd = len(out_shape)
+    shp = list(out_shape) + [1] * (MAX_DIMS - nd)
+    flat: List[int] = []
+    for j in range(3):
+        s = list(strides[j]) if j < len(strides) else []
+        s = s + [0] * (MAX_DIMS - len(s))
+        flat.extend(s)
+    return EW_GEOM.pack(*shp, *flat)
+
+
+def elementwise(dev: int, op: int, dtype_tag: int, ndim: int, n_in: int, ptrs, imms,
+                geometry: bytes, out_nbytes: int) -> DeviceBuffer:
+    desc = EW_HEAD.pack(op, dtype_tag, ndim, n_in, *ptrs, *imms) + geometry
+    out, ref = _outslot()
+    rc = _lib.sf_elementwise(dev, desc, ref)
+    if rc:
+        raise _err(_lib, rc, "elementwise")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def elementwise_into(dev: int, op: int, dtype_tag: int, ndim: int, n_in: int, ptrs, imms,
+                     geometry: bytes, out_ptr: int) -> None:
+    """Elementwise launch writing into an existing buffer (in-place updates)."""
+    desc = EW_HEAD.pack(op, dtype_tag, ndim, n_in, *ptrs, *imms) + geometry
+    out = ctypes.c_void_p(out_ptr)
+    rc = _lib.sf_elementwise(dev, desc, ctypes.byref(out))
+    if rc:
+        raise _err(_lib, rc, "elementwise")
+
+
+def reduce(dev: int, op: int, dtype_tag: int, shape, axes_mask: int, src: int,
+           out_nbytes: int) -> DeviceBuffer:
+    shp = struct.pack("<%dq" % len(shape), *shape) if shape else b"\0" * 8
+    out, ref = _outslot()
+    rc = _lib.sf_reduce(dev, op, dtype_tag, len(shape), shp, axes_mask, src, ref)
+    if rc:
+        raise _err(_lib, rc, "reduce")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def matmul(dev: int, dtype_tag: int, m: int, n: int, k: int, a: int, ta: int, b: int, tb: int,
+           out_nbytes: int) -> DeviceBuffer:
+    out, ref = _outslot()
+    rc = _lib.sf_matmul(dev, dtype_tag, m, n, k, a, ta, b, tb, ref)
+    if rc:
+        raise _err(_lib, rc, "matmul")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def transpose2d(dev: int, dtype_tag: int, rows: int, cols: int, src: int,
+                out_nbytes: int) -> DeviceBuffer:
+    out, ref = _outslot()
+    rc = _lib.sf_transpose2d(dev, dtype_tag, rows, cols, src, ref)
+    if rc:
+        raise _err(_lib, rc, "transpose")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def fill(dev: int, dtype_tag: int, n: int, value: float, out_nbytes: int) -> DeviceBuffer:
+    require_device()
+    out, ref = _outslot()
+    rc = _lib.sf_fill(dev, dtype_tag, n, value, ref)
+    if rc:
+        raise _err(_lib, rc, "fill")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def eye(dev: int, dtype_tag: int, n: int, out_nbytes: int) -> DeviceBuffer:
+    require_device()
+    out, ref = _outslot()
+    rc = _lib.sf_eye(dev, dtype_tag, n, ref)
+    if rc:
+        raise _err(_lib, rc, "eye")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def cast(dev: int, src_tag: int, dst_tag: int, n: int, src: int, out_nbytes: int) -> DeviceBuffer:
+    out, ref = _outslot()
+    rc = _lib.sf_cast(dev, src_tag, dst_tag, n, src, ref)
+    if rc:
+        raise _err(_lib, rc, "cast")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def rng(dev: int, kind: int, dtype_tag: int, n: int, out_nbytes: int) -> DeviceBuffer:
+    require_device()
+    out, ref = _outslot()
+    rc = _lib.sf_rng(dev, kind, dtype_tag, n, 0xFFFFFFFFFFFFFFFF, ref)
+    if rc:
+        raise _err(_lib, rc, "rng")
+    return DeviceBuffer(dev, out.value, out_nbytes)
+
+
+def dropout(dev: int, dtype_tag: int, n: int, x: int, u: int, u_tag: int, rate: float,
+            nbytes: int):
+    out, ref = _outslot()
+    m2 = _tls.out2
+    m2.value = None
+    rc = _lib.sf_dropout(dev, dtype_tag, n, x, u or None, u_tag, rate, ref, _tls.out2ref)
+    if rc:
+        raise _err(_lib, rc, "dropout")
+    return DeviceBuffer(dev, out.value, nbytes), DeviceBuffer(dev, m2.value, nbytes)
+
+
+# ---------------------------------------------------------------- JIT + plans
+def jit_compile(name: str, source: str) -> int:
+    L = load_library()
+    out = ctypes.c_void_p(0)
+    rc = L.sf_jit_compile(name.encode(), source.encode(), ctypes.byref(out))
+    if rc:
+        raise _err(L, rc, f"jit compile {name}")
+    return out.value
+
+
+class NativePlan:
+    """Owns a sf_plan handle (a lowered graph segment on one device)."""
+
+    __slots__ = ("handle", "dev", "n_in", "n_out", "_in_arr", "_out_arr", "n_launches",
+                 "_lock")
+
+    def __init__(self, dev: int, desc: bytes, n_in: int, n_out: int):
+        L = require_device()
+        h = ctypes.c_void_p(0)
+        rc = L.sf_plan_create(dev, desc, len(desc), ctypes.byref(h))
+        if rc:
+            raise _err(L, rc, "plan create")
+        self.handle = h.value
+        self.dev = dev
+        self.n_in = n_in
+        self.n_out = n_out
+        self._in_arr = (ctypes.c_void_p * max(1, n_in))()
+        self._out_arr = (ctypes.c_void_p * max(1, n_out))()
+        info = [ctypes.c_int(0) for _ in range(4)]
+        L.sf_plan_info(self.handle, *[ctypes.byref(x) for x in info])
+        self.n_launches = info[3].value
+        self._lock = threading.Lock()
+
+    def run(self, in_ptrs: Sequence[int]) -> List[int]:
+        with self._lock:
+            arr = self._in_arr
+            for i, p in enumerate(in_ptrs):
+                arr[i] = p
+            outs = self._out_arr
+            rc = _lib.sf_plan_run(self.handle, arr, outs)
+            if rc:
+                raise _err(_lib, rc, "plan run")
+            return outs[: self.n_out]
+
+    def __del__(self):
+        h = self.handle
+        if h:
+            self.handle = 0
+            try:
+                _lib.sf_plan_destroy(h)
+            except Exception:
+                pass

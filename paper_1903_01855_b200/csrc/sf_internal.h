@@ -1,0 +1,127 @@
+// sf_internal.h — shared internals of libsfb200.so (not part of the C-ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/sfb200.h"
+
+namespace sfrt {
+
+// Thread-local last error, returned by sf_last_error().
+void set_error(const std::string& msg);
+const char* last_error();
+
+#define SF_CHECK_CUDA(expr)                                                     \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::sfrt::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+      return SF_ERR_CUDA;                                                       \
+    }                                                                           \
+  } while (0)
+
+// Driver-API entry points, resolved through cudart at sf_init time so the
+// library has no link-time dependency on libcuda (it loads on GPU-less hosts,
+// where every entry point then fails with SF_ERR_NO_DEVICE).
+struct DriverApi {
+  CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*moduleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, unsigned, CUstream, void**, void**) = nullptr;
+};
+extern DriverApi drv;
+
+#define SF_CHECK_CU(expr)                                                       \
+  do {                                                                          \
+    CUresult _r = (expr);                                                       \
+    if (_r != CUDA_SUCCESS) {                                                   \
+      const char* _s = nullptr;                                                 \
+      if (::sfrt::drv.getErrorString) ::sfrt::drv.getErrorString(_r, &_s);      \
+      ::sfrt::set_error(std::string(#expr) + ": " + (_s ? _s : "?"));           \
+      return SF_ERR_CUDA;                                                       \
+    }                                                                           \
+  } while (0)
+
+#define SF_TRY(...)                  \
+  do {                               \
+    int _st = (__VA_ARGS__);         \
+    if (_st != SF_OK) return _st;    \
+  } while (0)
+
+// Size-class caching allocator: one per device, stream-ordered on the
+// device's single compute stream (a block freed after a launch may be
+// handed to the next launch without synchronisation, because both are
+// ordered on the same stream).
+class Allocator {
+ public:
+  int alloc(int dev, size_t bytes, void** p);
+  int release(void* p);
+  int trim();  // return cached blocks to the driver
+  size_t bytes_in_use() const { return in_use_; }
+  size_t bytes_cached() const { return cached_; }
+
+ private:
+  static size_t round_size(size_t bytes);
+  std::mutex mu_;
+  std::unordered_map<size_t, std::vector<void*>> free_;
+  std::unordered_map<void*, size_t> live_;
+  size_t in_use_ = 0, cached_ = 0;
+};
+
+struct Device {
+  int id = 0;
+  cudaStream_t stream = nullptr;
+  bool external_stream = false;
+  Allocator alloc;
+  // pinned staging ring for host->device copies: kStageSlots slots, each
+  // guarded by the event of the last transfer that read it
+  static constexpr int kStageSlots = 16;
+  static constexpr size_t kStageSlotBytes = 256u << 10;
+  std::mutex stage_mu;
+  char* pinned = nullptr;
+  cudaEvent_t slot_ready[kStageSlots] = {};
+  int next_slot = 0;
+  int sm_count = 0;
+  // device RNG (Philox) state: seed and next counter offset
+  unsigned long long rng_seed = 0;
+  unsigned long long rng_offset = 0;
+  std::mutex rng_mu;
+};
+
+Device* device(int dev);  // nullptr if invalid
+int ensure_device(int dev, Device** out);  // sets current device, validates
+size_t dtype_size(int dtype);
+void count_launch(int dev, unsigned long long n = 1);
+
+// Kernel launchers shared between the eager entry points and the plan
+// executor (all stream-ordered on d->stream).
+int launch_elementwise(Device* d, int op, int dtype, int ndim, const int64_t* shape,
+                       void* out, const void* const* ins, const int64_t* const* strides,
+                       const double* imms, int n_in);
+int launch_reduce(Device* d, int op, int dtype, int ndim, const int64_t* shape,
+                  uint32_t axes_mask, const void* in, void* out);
+int launch_matmul(Device* d, int dtype, int64_t m, int64_t n, int64_t k, const void* a,
+                  int trans_a, const void* b, int trans_b, void* c);
+int launch_transpose2d(Device* d, int dtype, int64_t rows, int64_t cols, const void* in,
+                       void* out);
+int launch_fill(Device* d, int dtype, int64_t n, double value, void* out);
+int launch_eye(Device* d, int dtype, int64_t n, void* out);
+int launch_rng(Device* d, int kind, int dtype, int64_t n, unsigned long long seed,
+               unsigned long long offset, void* out);
+int launch_dropout(Device* d, int dtype, int64_t n, const void* x, const void* u,
+                   int u_dtype, double rate, void* out, void* mask);
+int launch_cast(Device* d, int src_dtype, int dst_dtype, int64_t n, const void* in, void* out);
+
+}  // namespace sfrt

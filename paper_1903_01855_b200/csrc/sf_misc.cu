@@ -1,0 +1,216 @@
+// sf_misc.cu — transpose, fill/eye, device RNG, dropout.
+//
+// Reference kernels: _transpose_kernel (kernels.py:211-219), _eye_kernel
+// (:282-292), _random_normal_kernel (:372-384), _dropout_kernel (:387-404),
+// zeros_for/ones_for (gradients.py:65-76).
+#include "sf_internal.h"
+#include "sf_ops.cuh"
+
+namespace sfrt {
+
+static unsigned grid_n(Device* d, long long n) {
+  long long b = (n + 255) / 256;
+  const long long cap = (long long)d->sm_count * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// 32x32 tiles through shared memory (coalesced both ways).
+template <class T>
+__global__ void transpose_tiled(const T* __restrict__ in, T* __restrict__ out, long long rows,
+                                long long cols) {
+  __shared__ T tile[32][33];
+  const long long bx = (long long)blockIdx.x * 32, by = (long long)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long long r = by + j, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long long r = bx + j, c = by + threadIdx.x;  // out is cols x rows
+    if (r < cols && c < rows) out[r * rows + c] = tile[threadIdx.x][j];
+  }
+}
+
+template <class T>
+static void transpose_go(Device* d, const T* in, T* out, long long rows, long long cols) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_tiled<T><<<grid, dim3(32, 8), 0, d->stream>>>(in, out, rows, cols);
+}
+
+int launch_transpose2d(Device* d, int dtype, int64_t rows, int64_t cols, const void* in, void* out) {
+  if (rows == 0 || cols == 0) return SF_OK;
+  count_launch(d->id);
+  switch (dtype_size(dtype)) {
+    case 1: transpose_go<unsigned char>(d, (const unsigned char*)in, (unsigned char*)out, rows, cols); break;
+    case 4: transpose_go<unsigned>(d, (const unsigned*)in, (unsigned*)out, rows, cols); break;
+    case 8: transpose_go<unsigned long long>(d, (const unsigned long long*)in, (unsigned long long*)out, rows, cols); break;
+    default: set_error("transpose: bad dtype"); return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class T>
+__global__ void fill_kernel(T* __restrict__ out, long long n, T v) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) out[i] = v;
+}
+
+int launch_fill(Device* d, int dtype, int64_t n, double value, void* out) {
+  if (n == 0) return SF_OK;
+  count_launch(d->id);
+  const unsigned g = grid_n(d, n);
+  switch (dtype) {
+    case SF_DTYPE_F32: fill_kernel<float><<<g, 256, 0, d->stream>>>((float*)out, n, (float)value); break;
+    case SF_DTYPE_F64: fill_kernel<double><<<g, 256, 0, d->stream>>>((double*)out, n, value); break;
+    case SF_DTYPE_I32: fill_kernel<int><<<g, 256, 0, d->stream>>>((int*)out, n, (int)value); break;
+    case SF_DTYPE_BOOL: fill_kernel<bool><<<g, 256, 0, d->stream>>>((bool*)out, n, value != 0.0); break;
+    default: set_error("fill: bad dtype"); return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class T>
+__global__ void eye_kernel(T* __restrict__ out, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n * n; i += stride)
+    out[i] = (i / n == i % n) ? T(1) : T(0);
+}
+
+int launch_eye(Device* d, int dtype, int64_t n, void* out) {
+  if (n == 0) return SF_OK;
+  count_launch(d->id);
+  const unsigned g = grid_n(d, n * n);
+  switch (dtype) {
+    case SF_DTYPE_F32: eye_kernel<float><<<g, 256, 0, d->stream>>>((float*)out, n); break;
+    case SF_DTYPE_F64: eye_kernel<double><<<g, 256, 0, d->stream>>>((double*)out, n); break;
+    default: set_error("eye produces float tensors"); return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class T>
+__global__ void rng_kernel(T* __restrict__ out, long long n, int kind, unsigned long long seed,
+                           unsigned long long offset) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned long long ctr = offset + (unsigned long long)i;
+    if (kind == 0) out[i] = (T)sf::normal_f64(ctr, seed);
+    else out[i] = sizeof(T) == 4 ? (T)sf::uniform_f32(ctr, seed) : (T)sf::uniform_f64(ctr, seed);
+  }
+}
+
+int launch_rng(Device* d, int kind, int dtype, int64_t n, unsigned long long seed,
+               unsigned long long offset, void* out) {
+  if (n == 0) return SF_OK;
+  count_launch(d->id);
+  const unsigned g = grid_n(d, n);
+  switch (dtype) {
+    case SF_DTYPE_F32: rng_kernel<float><<<g, 256, 0, d->stream>>>((float*)out, n, kind, seed, offset); break;
+    case SF_DTYPE_F64: rng_kernel<double><<<g, 256, 0, d->stream>>>((double*)out, n, kind, seed, offset); break;
+    default: set_error("rng produces float tensors"); return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+// mask = (u >= rate) / keep ; out = x * mask   (u: f64 or f32 uniforms, or
+// device Philox draws when u == NULL)
+template <class T, class U>
+__global__ void dropout_kernel(const T* __restrict__ x, const U* __restrict__ u, long long n,
+                               double rate, T keep, unsigned long long seed,
+                               unsigned long long offset, T* __restrict__ out,
+                               T* __restrict__ mask) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double ui = u ? (double)u[i] : sf::uniform_f64(offset + (unsigned long long)i, seed);
+    const T m = (ui >= rate ? T(1) : T(0)) / keep;
+    mask[i] = m;
+    out[i] = x[i] * m;
+  }
+}
+
+int launch_dropout(Device* d, int dtype, int64_t n, const void* x, const void* u, int u_dtype,
+                   double rate, void* out, void* mask) {
+  if (n == 0) return SF_OK;
+  unsigned long long offset = 0;
+  if (!u) {
+    std::lock_guard<std::mutex> lk(d->rng_mu);
+    offset = d->rng_offset;
+    d->rng_offset += (unsigned long long)n;
+  }
+  count_launch(d->id);
+  const unsigned g = grid_n(d, n);
+  const double keep = 1.0 - rate;
+  const unsigned long long seed = d->rng_seed;
+  if (dtype == SF_DTYPE_F32) {
+    if (u_dtype == SF_DTYPE_F32)
+      dropout_kernel<float, float><<<g, 256, 0, d->stream>>>((const float*)x, (const float*)u, n, rate, (float)keep, seed, offset, (float*)out, (float*)mask);
+    else
+      dropout_kernel<float, double><<<g, 256, 0, d->stream>>>((const float*)x, (const double*)u, n, rate, (float)keep, seed, offset, (float*)out, (float*)mask);
+  } else if (dtype == SF_DTYPE_F64) {
+    if (u_dtype == SF_DTYPE_F32)
+      dropout_kernel<double, float><<<g, 256, 0, d->stream>>>((const double*)x, (const float*)u, n, rate, keep, seed, offset, (double*)out, (double*)mask);
+    else
+      dropout_kernel<double, double><<<g, 256, 0, d->stream>>>((const double*)x, (const double*)u, n, rate, keep, seed, offset, (double*)out, (double*)mask);
+  } else {
+    set_error("dropout requires a float tensor");
+    return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+}  // namespace sfrt
+
+using namespace sfrt;
+
+extern "C" {
+
+int sf_transpose2d(int dev, int dtype, int64_t rows, int64_t cols, const void* in, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(rows * cols) * dtype_size(dtype), out));
+  return launch_transpose2d(d, dtype, rows, cols, in, *out);
+}
+
+int sf_fill(int dev, int dtype, int64_t n, double value, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * dtype_size(dtype), out));
+  return launch_fill(d, dtype, n, value, *out);
+}
+
+int sf_eye(int dev, int dtype, int64_t n, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(n * n) * dtype_size(dtype), out));
+  return launch_eye(d, dtype, n, *out);
+}
+
+int sf_rng(int dev, int kind, int dtype, int64_t n, uint64_t offset, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (offset == UINT64_MAX) {
+    std::lock_guard<std::mutex> lk(d->rng_mu);
+    offset = d->rng_offset;
+    d->rng_offset += (uint64_t)n;
+  }
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * dtype_size(dtype), out));
+  return launch_rng(d, kind, dtype, n, d->rng_seed, offset, *out);
+}
+
+int sf_dropout(int dev, int dtype, int64_t n, const void* x, const void* u, int u_dtype,
+               double rate, void** out, void** mask) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * dtype_size(dtype), out));
+  if (*mask == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * dtype_size(dtype), mask));
+  return launch_dropout(d, dtype, n, x, u, u_dtype, rate, *out, *mask);
+}
+
+}  // extern "C"

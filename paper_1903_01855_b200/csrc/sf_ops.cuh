@@ -1,0 +1,281 @@
+// sf_ops.cuh — scalar semantics of every elementwise primitive.
+//
+// This header is the single definition of per-element arithmetic for the
+// backend.  It is compiled twice: by nvcc into the ahead-of-time eager
+// kernels (libsfb200.so) and, embedded as a string, by NVRTC into the fused
+// kernels generated for staged graph functions.  Both compilations use the
+// same IEEE flags (-fmad=false, -prec-div=true, -prec-sqrt=true, -ftz=false),
+// which is what makes an eager op and the same op inside a fused staged
+// kernel produce identical bits — the GPU restatement of the reference's
+// "one kernel shared by both execution modes" rule
+// (reference: stageflow/kernels.py:1-11).
+//
+// NumPy edge semantics mirrored here (reference kernels: stageflow/kernels.py):
+//   relu      = np.maximum(x, 0): NaN propagates, -0.0 -> +0.0      (:176-177)
+//   softplus  = np.logaddexp(0.0, x) incl. its x==0 branch           (:171-173)
+//   step_pos  = (x > 0) as float                                     (:180-181)
+//   int32 add/sub/mul/neg wrap modulo 2^32                           (:116-153)
+//   exp overflow -> inf, log(0) -> -inf, log(<0) -> nan              (:161-168)
+#pragma once
+
+#ifndef SF_DEVFN
+#define SF_DEVFN __device__ __forceinline__
+#endif
+
+// ---- dtype tags (same numbering as the reference wire tags, dtypes.py:63-69)
+#define SF_F32 1
+#define SF_F64 2
+#define SF_I32 3
+#define SF_BOOL 4
+
+// ---- opcodes (mirrored in paper_1903_01855_b200/_native.py) ----------------
+// unary
+#define SF_OP_IDENTITY 0
+#define SF_OP_NEG 1
+#define SF_OP_EXP 2
+#define SF_OP_LOG 3
+#define SF_OP_SOFTPLUS 4
+#define SF_OP_RELU 5
+#define SF_OP_STEP_POS 6
+#define SF_OP_TANH 7
+#define SF_OP_SQRT 8
+#define SF_OP_RSQRT 9
+#define SF_OP_SIGMOID 10
+#define SF_OP_ABS 11
+#define SF_OP_SQUARE 12
+#define SF_OP_ISFINITE 13
+#define SF_OP_LOGICAL_NOT 14
+#define SF_OP_RECIPROCAL 15
+#define SF_OP_COS 16
+#define SF_OP_SIN 17
+// binary
+#define SF_OP_ADD 32
+#define SF_OP_SUB 33
+#define SF_OP_MUL 34
+#define SF_OP_DIV 35
+#define SF_OP_GREATER 36
+#define SF_OP_MAXIMUM 37
+#define SF_OP_MINIMUM 38
+#define SF_OP_LESS 39
+#define SF_OP_EQUAL 40
+#define SF_OP_GREATER_EQUAL 41
+// ternary
+#define SF_OP_SELECT 64
+
+#define SF_OP_IS_BINARY(op) ((op) >= 32 && (op) < 64)
+#define SF_OP_IS_TERNARY(op) ((op) >= 64)
+
+namespace sf {
+
+// ------------------------------------------------------------------ float32
+SF_DEVFN float neg(float x) { return -x; }
+SF_DEVFN float exp_(float x) { return expf(x); }
+SF_DEVFN float log_(float x) { return logf(x); }
+SF_DEVFN float softplus(float x) {
+  // np.logaddexp(0.0, x) (npy_logaddexp with a = 0, b = x)
+  if (x == 0.0f) return 0.0f + 0.693147180559945309417232121458176568f;
+  const float t = 0.0f - x;
+  if (t > 0.0f) return 0.0f + log1pf(expf(x));
+  if (t <= 0.0f) return x + log1pf(expf(t));
+  return t;  // NaN
+}
+SF_DEVFN float relu(float x) { return x > 0.0f ? x : (x != x ? x : 0.0f); }
+SF_DEVFN float step_pos(float x) { return x > 0.0f ? 1.0f : 0.0f; }
+SF_DEVFN float tanh_(float x) { return tanhf(x); }
+SF_DEVFN float sqrt_(float x) { return sqrtf(x); }
+SF_DEVFN float rsqrt_(float x) { return 1.0f / sqrtf(x); }
+SF_DEVFN float sigmoid(float x) { return 1.0f / (1.0f + expf(-x)); }
+SF_DEVFN float abs_(float x) { return fabsf(x); }
+SF_DEVFN float square(float x) { return x * x; }
+SF_DEVFN float recip(float x) { return 1.0f / x; }
+SF_DEVFN float cos_(float x) { return cosf(x); }
+SF_DEVFN float sin_(float x) { return sinf(x); }
+SF_DEVFN bool isfinite_(float x) { return isfinite(x); }
+SF_DEVFN float add(float a, float b) { return a + b; }
+SF_DEVFN float sub(float a, float b) { return a - b; }
+SF_DEVFN float mul(float a, float b) { return a * b; }
+SF_DEVFN float div(float a, float b) { return a / b; }
+// np.maximum / np.minimum propagate NaN from either side.
+SF_DEVFN float maximum(float a, float b) { return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b)); }
+SF_DEVFN float minimum(float a, float b) { return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b)); }
+
+// ------------------------------------------------------------------ float64
+SF_DEVFN double neg(double x) { return -x; }
+SF_DEVFN double exp_(double x) { return exp(x); }
+SF_DEVFN double log_(double x) { return log(x); }
+SF_DEVFN double softplus(double x) {
+  if (x == 0.0) return 0.0 + 0.693147180559945309417232121458176568;
+  const double t = 0.0 - x;
+  if (t > 0.0) return 0.0 + log1p(exp(x));
+  if (t <= 0.0) return x + log1p(exp(t));
+  return t;
+}
+SF_DEVFN double relu(double x) { return x > 0.0 ? x : (x != x ? x : 0.0); }
+SF_DEVFN double step_pos(double x) { return x > 0.0 ? 1.0 : 0.0; }
+SF_DEVFN double tanh_(double x) { return tanh(x); }
+SF_DEVFN double sqrt_(double x) { return sqrt(x); }
+SF_DEVFN double rsqrt_(double x) { return 1.0 / sqrt(x); }
+SF_DEVFN double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+SF_DEVFN double abs_(double x) { return fabs(x); }
+SF_DEVFN double square(double x) { return x * x; }
+SF_DEVFN double recip(double x) { return 1.0 / x; }
+SF_DEVFN double cos_(double x) { return cos(x); }
+SF_DEVFN double sin_(double x) { return sin(x); }
+SF_DEVFN bool isfinite_(double x) { return isfinite(x); }
+SF_DEVFN double add(double a, double b) { return a + b; }
+SF_DEVFN double sub(double a, double b) { return a - b; }
+SF_DEVFN double mul(double a, double b) { return a * b; }
+SF_DEVFN double div(double a, double b) { return a / b; }
+SF_DEVFN double maximum(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b)); }
+SF_DEVFN double minimum(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b)); }
+
+// ------------------------------------------------------------------ int32 (wrapping)
+SF_DEVFN int neg(int x) { return (int)(0u - (unsigned)x); }
+SF_DEVFN int add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
+SF_DEVFN int sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }
+SF_DEVFN int mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
+SF_DEVFN int abs_(int x) { return x < 0 ? neg(x) : x; }
+SF_DEVFN int square(int x) { return mul(x, x); }
+SF_DEVFN int maximum(int a, int b) { return a >= b ? a : b; }
+SF_DEVFN int minimum(int a, int b) { return a <= b ? a : b; }
+SF_DEVFN int relu(int x) { return x > 0 ? x : 0; }
+SF_DEVFN int step_pos(int x) { return x > 0 ? 1 : 0; }
+SF_DEVFN bool isfinite_(int) { return true; }
+
+// ------------------------------------------------------------------ generic dispatch
+// Used by the AOT eager kernels; the fused code generator calls the named
+// functions above directly (same code, so the same bits).
+template <class T>
+SF_DEVFN T unary_f(int op, T x) {
+  switch (op) {
+    case SF_OP_IDENTITY: return x;
+    case SF_OP_NEG: return neg(x);
+    case SF_OP_EXP: return exp_(x);
+    case SF_OP_LOG: return log_(x);
+    case SF_OP_SOFTPLUS: return softplus(x);
+    case SF_OP_RELU: return relu(x);
+    case SF_OP_STEP_POS: return step_pos(x);
+    case SF_OP_TANH: return tanh_(x);
+    case SF_OP_SQRT: return sqrt_(x);
+    case SF_OP_RSQRT: return rsqrt_(x);
+    case SF_OP_SIGMOID: return sigmoid(x);
+    case SF_OP_ABS: return abs_(x);
+    case SF_OP_SQUARE: return square(x);
+    case SF_OP_RECIPROCAL: return recip(x);
+    case SF_OP_COS: return cos_(x);
+    case SF_OP_SIN: return sin_(x);
+    default: return x;
+  }
+}
+template <>
+SF_DEVFN int unary_f<int>(int op, int x) {
+  switch (op) {
+    case SF_OP_IDENTITY: return x;
+    case SF_OP_NEG: return neg(x);
+    case SF_OP_ABS: return abs_(x);
+    case SF_OP_SQUARE: return square(x);
+    case SF_OP_RELU: return relu(x);
+    case SF_OP_STEP_POS: return step_pos(x);
+    default: return x;
+  }
+}
+
+template <class T>
+SF_DEVFN T binary_f(int op, T a, T b) {
+  switch (op) {
+    case SF_OP_ADD: return add(a, b);
+    case SF_OP_SUB: return sub(a, b);
+    case SF_OP_MUL: return mul(a, b);
+    case SF_OP_DIV: return div(a, b);
+    case SF_OP_MAXIMUM: return maximum(a, b);
+    case SF_OP_MINIMUM: return minimum(a, b);
+    default: return a;
+  }
+}
+template <>
+SF_DEVFN int binary_f<int>(int op, int a, int b) {
+  switch (op) {
+    case SF_OP_ADD: return add(a, b);
+    case SF_OP_SUB: return sub(a, b);
+    case SF_OP_MUL: return mul(a, b);
+    case SF_OP_MAXIMUM: return maximum(a, b);
+    case SF_OP_MINIMUM: return minimum(a, b);
+    default: return a;
+  }
+}
+
+// boolean tensors only support identity/copy and equality
+template <>
+SF_DEVFN bool unary_f<bool>(int op, bool x) { return x; }
+template <>
+SF_DEVFN bool binary_f<bool>(int op, bool a, bool b) { return a; }
+
+template <class T>
+SF_DEVFN bool compare_f(int op, T a, T b) {
+  switch (op) {
+    case SF_OP_GREATER: return a > b;
+    case SF_OP_LESS: return a < b;
+    case SF_OP_EQUAL: return a == b;
+    case SF_OP_GREATER_EQUAL: return a >= b;
+    default: return false;
+  }
+}
+
+// ------------------------------------------------------------------ reductions
+// Canonical reduction order (CRO), shared by the eager reduce kernel and the
+// fused row programs.  For n elements: lane l (0..31) folds x[l], x[l+32],
+// x[l+64], ... left to right; the 32 partials are then combined by the xor
+// butterfly (offsets 16, 8, 4, 2, 1) and lane 0's value is the result.  An
+// empty partial is "absent" (not +0.0), so a single -0.0 sums to -0.0 like
+// NumPy.  Longer reductions (n > SF_CRO_CHUNK) first reduce each
+// SF_CRO_CHUNK-element chunk with the CRO, then reduce the chunk results
+// with the CRO.  NumPy itself sums pairwise; the reference-vs-GPU contract
+// for floats is therefore rtol-based (SURVEY.md §7 hard part (i)).
+#define SF_CRO_CHUNK 8192
+
+// ------------------------------------------------------------------ RNG
+// Philox4x32-10, counter-based: element i of a draw with (seed, offset)
+// uses counter (offset + i, 0, 0, 0) and key (seed_lo, seed_hi).  Eager and
+// fused kernels evaluate the same function, so eager == staged for the
+// device RNG mode.
+struct u4 { unsigned x, y, z, w; };
+SF_DEVFN u4 philox(unsigned long long ctr, unsigned long long seed) {
+  unsigned c0 = (unsigned)ctr, c1 = (unsigned)(ctr >> 32), c2 = 0u, c3 = 0u;
+  unsigned k0 = (unsigned)seed, k1 = (unsigned)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  u4 r;
+  r.x = c0; r.y = c1; r.z = c2; r.w = c3;
+  return r;
+}
+// uniform in [0, 1)
+SF_DEVFN float uniform_f32(unsigned long long ctr, unsigned long long seed) {
+  const u4 r = philox(ctr, seed);
+  return (float)(r.x >> 8) * 5.9604644775390625e-08f;  // 2^-24
+}
+SF_DEVFN double uniform_f64(unsigned long long ctr, unsigned long long seed) {
+  const u4 r = philox(ctr, seed);
+  const unsigned long long m = ((unsigned long long)(r.x >> 5) << 26) | (r.y >> 6);
+  return (double)m * 1.1102230246251565e-16;  // 2^-53
+}
+// standard normal via Box-Muller on two 53-bit uniforms (computed in f64,
+// rounded once to the output dtype).
+SF_DEVFN double normal_f64(unsigned long long ctr, unsigned long long seed) {
+  const u4 r = philox(ctr, seed);
+  const unsigned long long m1 = ((unsigned long long)(r.x >> 5) << 26) | (r.y >> 6);
+  const unsigned long long m2 = ((unsigned long long)(r.z >> 5) << 26) | (r.w >> 6);
+  const double u1 = ((double)m1 + 1.0) * 1.1102230246251565e-16;  // (0, 1]
+  const double u2 = (double)m2 * 1.1102230246251565e-16;
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+}  // namespace sf

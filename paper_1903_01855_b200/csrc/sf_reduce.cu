@@ -1,0 +1,321 @@
+// sf_reduce.cu — reduce_sum / reduce_mean over arbitrary axes.
+//
+// Reference: _reduce_kernel (np.sum / np.mean), stageflow/kernels.py:323-364.
+// Summation follows the canonical reduction order (CRO) defined in
+// sf_ops.cuh, which depends only on the reduced length, so the eager kernel
+// and any fused staged kernel that inlines a reduction agree bit-for-bit.
+//
+// dtype semantics mirrored from NumPy:
+//   f32/f64 sum accumulates in the input dtype; mean = sum / count in dtype.
+//   i32 sum wraps modulo 2^32 (numpy accumulates in int64, _wrap casts back).
+//   i32 mean (eager only; staged inference rejects it, kernels.py:344-352)
+//   accumulates in f64, divides, truncates to int32 like the astype in _wrap.
+#include "sf_internal.h"
+#include "sf_ops.cuh"
+
+namespace sfrt {
+
+struct RedArgs {
+  long long n_out;     // kept elements
+  long long r;         // reduced elements per output
+  long long chunk;     // elements per chunk (SF_CRO_CHUNK or r)
+  long long n_chunks;  // chunks per output
+  int kept_nd, red_nd;
+  long long kept_shape[SF_MAX_DIMS], kept_stride[SF_MAX_DIMS];
+  long long red_shape[SF_MAX_DIMS], red_stride[SF_MAX_DIMS];
+};
+
+template <class T>
+struct Acc { typedef T type; };
+template <>
+struct Acc<int> { typedef unsigned type; };
+
+template <class A>
+__device__ __forceinline__ A cadd(A a, A b) { return a + b; }
+
+__device__ __forceinline__ long long kept_offset(const RedArgs& a, long long o) {
+  long long off = 0;
+#pragma unroll
+  for (int d = SF_MAX_DIMS - 1; d >= 0; --d) {
+    if (d < a.kept_nd) {
+      const long long e = a.kept_shape[d];
+      off += (o % e) * a.kept_stride[d];
+      o /= e;
+    }
+  }
+  return off;
+}
+
+__device__ __forceinline__ long long red_offset(const RedArgs& a, long long j) {
+  if (a.red_nd == 1) return j * a.red_stride[0];
+  long long off = 0;
+#pragma unroll
+  for (int d = SF_MAX_DIMS - 1; d >= 0; --d) {
+    if (d < a.red_nd) {
+      const long long e = a.red_shape[d];
+      off += (j % e) * a.red_stride[d];
+      j /= e;
+    }
+  }
+  return off;
+}
+
+// One warp per (output, chunk).  Lane l folds elements l, l+32, ... of the
+// chunk left to right, then the xor butterfly combines the lanes (lanes with
+// no element are absent).  Writes the chunk partial (A) to part.
+template <class T, class A>
+__global__ void reduce_chunks(const RedArgs a, const T* __restrict__ in, A* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       w < a.n_out * a.n_chunks; w += warps) {
+    const long long o = w / a.n_chunks, c = w % a.n_chunks;
+    const long long base = kept_offset(a, o);
+    const long long j0 = c * a.chunk;
+    long long len = a.r - j0;
+    if (len > a.chunk) len = a.chunk;
+    A acc = A();
+    bool present = false;
+    for (long long j = lane; j < len; j += 32) {
+      const A v = (A)in[base + red_offset(a, j0 + j)];
+      acc = present ? cadd(acc, v) : v;
+      present = true;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const A ov = __shfl_xor_sync(0xffffffffu, acc, off);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, off);
+      if (present && op) acc = cadd(acc, ov);
+      else if (op) acc = ov;
+      present = present || op;
+    }
+    if (lane == 0) part[w] = acc;
+  }
+}
+
+// Sequential CRO over <= 32 values per output, one thread per output; used
+// for short reductions (r <= 32) and for the second level over chunk
+// partials.  Identical tree to the warp butterfly above.
+template <class A>
+__device__ __forceinline__ A cro_small(A* acc, int p) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+    for (int l = 0; l < off; ++l)
+      if (l + off < p) acc[l] = cadd(acc[l], acc[l + off]);
+  }
+  return acc[0];
+}
+
+template <class T, class A>
+__global__ void reduce_short(const RedArgs a, const T* __restrict__ in, A* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < a.n_out; o += stride) {
+    const long long base = kept_offset(a, o);
+    A acc[32];
+    const int p = (int)a.r;
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+      if (l < p) acc[l] = (A)in[base + red_offset(a, l)];
+    out[o] = p > 0 ? cro_small(acc, p) : A();
+  }
+}
+
+// Second level: CRO over the n_chunks partials of each output (any count).
+template <class A>
+__global__ void reduce_partials(const A* __restrict__ part, long long n_out, long long n_chunks,
+                                A* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long o = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); o < n_out;
+       o += warps) {
+    A acc = A();
+    bool present = false;
+    for (long long j = lane; j < n_chunks; j += 32) {
+      const A v = part[o * n_chunks + j];
+      acc = present ? cadd(acc, v) : v;
+      present = true;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const A ov = __shfl_xor_sync(0xffffffffu, acc, off);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, off);
+      if (present && op) acc = cadd(acc, ov);
+      else if (op) acc = ov;
+      present = present || op;
+    }
+    if (lane == 0) out[o] = acc;
+  }
+}
+
+// Finalise: out = cast(sum) or cast(sum / count).
+template <class A, class T>
+__global__ void reduce_finalize(const A* __restrict__ sums, long long n, int mean, double count,
+                                T* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (mean) out[i] = (T)(sums[i] / (A)count);
+    else out[i] = (T)sums[i];
+  }
+}
+// int32 mean: f64 accumulate, divide, truncate (numpy astype semantics).
+__global__ void reduce_finalize_i32_mean(const double* __restrict__ sums, long long n,
+                                         double count, int* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double q = sums[i] / count;
+    if (q != q) q = 0.0;
+    if (q >= 2147483648.0) q = -2147483648.0;  // x86 cvttsd2si overflow result
+    if (q < -2147483648.0) q = -2147483648.0;
+    out[i] = (int)q;
+  }
+}
+
+static unsigned grid_cap(Device* d, long long threads) {
+  long long b = (threads + 255) / 256;
+  const long long cap = (long long)d->sm_count * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+template <class T, class A>
+static int run_reduce(Device* d, const RedArgs& a, const T* in, A* sums) {
+  if (a.r <= 32) {
+    reduce_short<T, A><<<grid_cap(d, a.n_out), 256, 0, d->stream>>>(a, in, sums);
+    count_launch(d->id);
+    return SF_OK;
+  }
+  if (a.n_chunks == 1) {
+    reduce_chunks<T, A><<<grid_cap(d, a.n_out * 32), 256, 0, d->stream>>>(a, in, sums);
+    count_launch(d->id);
+    return SF_OK;
+  }
+  A* part = nullptr;
+  SF_TRY(d->alloc.alloc(d->id, sizeof(A) * a.n_out * a.n_chunks, (void**)&part));
+  reduce_chunks<T, A><<<grid_cap(d, a.n_out * a.n_chunks * 32), 256, 0, d->stream>>>(a, in, part);
+  reduce_partials<A><<<grid_cap(d, a.n_out * 32), 256, 0, d->stream>>>(part, a.n_out, a.n_chunks, sums);
+  count_launch(d->id, 2);
+  d->alloc.release(part);  // stream-ordered reuse is safe
+  return SF_OK;
+}
+
+int launch_reduce(Device* d, int op, int dtype, int ndim, const int64_t* shape,
+                  uint32_t axes_mask, const void* in, void* out) {
+  RedArgs a;
+  std::memset(&a, 0, sizeof(a));
+  long long stride[SF_MAX_DIMS];
+  long long s = 1;
+  for (int i = ndim - 1; i >= 0; --i) {
+    stride[i] = s;
+    s *= shape[i];
+  }
+  a.n_out = 1;
+  a.r = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (shape[i] == 1) continue;  // size-1 dims do not affect either side
+    if (axes_mask & (1u << i)) {
+      // merge with the previous reduced dim if contiguous
+      if (a.red_nd > 0 && a.red_stride[a.red_nd - 1] == stride[i] * shape[i]) {
+        a.red_shape[a.red_nd - 1] *= shape[i];
+        a.red_stride[a.red_nd - 1] = stride[i];
+      } else {
+        a.red_shape[a.red_nd] = shape[i];
+        a.red_stride[a.red_nd] = stride[i];
+        ++a.red_nd;
+      }
+      a.r *= shape[i];
+    } else {
+      if (a.kept_nd > 0 && a.kept_stride[a.kept_nd - 1] == stride[i] * shape[i]) {
+        a.kept_shape[a.kept_nd - 1] *= shape[i];
+        a.kept_stride[a.kept_nd - 1] = stride[i];
+      } else {
+        a.kept_shape[a.kept_nd] = shape[i];
+        a.kept_stride[a.kept_nd] = stride[i];
+        ++a.kept_nd;
+      }
+      a.n_out *= shape[i];
+    }
+  }
+  long long total = 1;
+  for (int i = 0; i < ndim; ++i) total *= shape[i];
+  if (total == 0) {
+    // empty reduction: sum -> 0, mean -> nan (numpy), or empty output
+    long long n_out = 1;
+    for (int i = 0; i < ndim; ++i)
+      if (!(axes_mask & (1u << i))) n_out *= shape[i];
+    if (n_out == 0) return SF_OK;
+    const double v = op == 1 ? (dtype == SF_DTYPE_I32 ? -2147483648.0 : __builtin_nan("")) : 0.0;
+    return launch_fill(d, dtype, n_out, v, out);
+  }
+  if (a.red_nd == 0) a.red_shape[0] = 1, a.red_stride[0] = 1, a.red_nd = 1;
+  a.chunk = a.r > SF_CRO_CHUNK ? SF_CRO_CHUNK : a.r;
+  a.n_chunks = (a.r + a.chunk - 1) / a.chunk;
+  const double count = (double)a.r;
+  const unsigned gf = grid_cap(d, a.n_out);
+  switch (dtype) {
+    case SF_DTYPE_F32: {
+      if (op == 0) {
+        SF_TRY(run_reduce<float, float>(d, a, (const float*)in, (float*)out));
+      } else {
+        float* sums = nullptr;
+        SF_TRY(d->alloc.alloc(d->id, sizeof(float) * a.n_out, (void**)&sums));
+        SF_TRY(run_reduce<float, float>(d, a, (const float*)in, sums));
+        reduce_finalize<float, float><<<gf, 256, 0, d->stream>>>(sums, a.n_out, 1, count, (float*)out);
+        count_launch(d->id);
+        d->alloc.release(sums);
+      }
+      break;
+    }
+    case SF_DTYPE_F64: {
+      if (op == 0) {
+        SF_TRY(run_reduce<double, double>(d, a, (const double*)in, (double*)out));
+      } else {
+        double* sums = nullptr;
+        SF_TRY(d->alloc.alloc(d->id, sizeof(double) * a.n_out, (void**)&sums));
+        SF_TRY(run_reduce<double, double>(d, a, (const double*)in, sums));
+        reduce_finalize<double, double><<<gf, 256, 0, d->stream>>>(sums, a.n_out, 1, count, (double*)out);
+        count_launch(d->id);
+        d->alloc.release(sums);
+      }
+      break;
+    }
+    case SF_DTYPE_I32: {
+      if (op == 0) {
+        SF_TRY(run_reduce<int, unsigned>(d, a, (const int*)in, (unsigned*)out));
+      } else {
+        double* sums = nullptr;
+        SF_TRY(d->alloc.alloc(d->id, sizeof(double) * a.n_out, (void**)&sums));
+        SF_TRY(run_reduce<int, double>(d, a, (const int*)in, sums));
+        reduce_finalize_i32_mean<<<gf, 256, 0, d->stream>>>(sums, a.n_out, count, (int*)out);
+        count_launch(d->id);
+        d->alloc.release(sums);
+      }
+      break;
+    }
+    default:
+      set_error("reduce: not defined for this dtype");
+      return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+}  // namespace sfrt
+
+using namespace sfrt;
+
+extern "C" int sf_reduce(int dev, int op, int dtype, int ndim, const int64_t* shape,
+                         uint32_t axes_mask, const void* in, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (ndim < 0 || ndim > SF_MAX_DIMS) {
+    set_error("sf_reduce: bad rank");
+    return SF_ERR_INVALID;
+  }
+  long long n_out = 1;
+  for (int i = 0; i < ndim; ++i)
+    if (!(axes_mask & (1u << i))) n_out *= shape[i];
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n_out * dtype_size(dtype), out));
+  return launch_reduce(d, op, dtype, ndim, shape, axes_mask, in, *out);
+}

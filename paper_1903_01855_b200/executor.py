@@ -1,0 +1,502 @@
+"""Execution of graph functions (reference: stageflow/executor.py).
+
+``execute_graph`` validates the bound inputs exactly like the reference
+(:153-193), then runs the graph's *native program*: the lowered, fused form
+built by lowering.py once per (device, input signature) and cached on
+``gf._plan``.  A program is a sequence of segments — native plans (one
+``sf_plan_run`` each) and the few nodes that must run through Python
+(host callbacks, tensor-dependent control flow, plugin ops without a
+lowering, host-RNG parity draws).
+
+Graphs that pin nodes to other devices on a multi-GPU runtime run through
+``_interpret`` instead: per-node launches with the reference's transparent
+copy accounting (:231-261), so copy counters stay identical.
+"""
+from __future__ import annotations
+
+import struct
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _native, dtypes
+from .dtypes import DType
+from .errors import (CallbackError, DeadVariable, InputMismatch, KernelError, MissingFunction,
+                     NotSerializable, SignatureViolation, StageflowError)
+from .graph import GraphFunction, Node
+from .kernels import KernelEnv, ordinal_of, relabel
+from .lowering import (FusedGroup, LOp, Lowerer, LV, PlanWriter, SLOT_CONST, SLOT_INPUT,
+                       SLOT_OUTPUT, SLOT_TEMP, fuse, generate_group, pack_ew_step)
+from .runtime import current_context, get_runtime
+from .tensor import Tensor
+
+_PASSTHROUGH = (CallbackError, SignatureViolation, DeadVariable, MissingFunction, InputMismatch,
+                NotSerializable)
+
+
+def _known(shape) -> bool:
+    return None not in tuple(shape)
+
+
+def _bind_inputs(gf: GraphFunction, values: Sequence) -> None:
+    from .state import Variable
+
+    if len(values) != len(gf.inputs):
+        raise InputMismatch(f"{gf.name} takes {len(gf.inputs)} inputs (including captures), "
+                            f"got {len(values)}")
+    for ph, v in zip(gf.inputs, values):
+        if ph.is_variable_ref or isinstance(v, Variable):
+            if not isinstance(v, Variable):
+                raise InputMismatch(f"{gf.name}: input {ph.name!r} expects a variable")
+            if v.dtype is not ph.dtype or (_known(ph.shape) and v.shape != ph.shape):
+                raise InputMismatch(
+                    f"{gf.name}: variable bound to {ph.name!r} is {v.dtype.value}{list(v.shape)}, "
+                    f"expected {ph.dtype.value}{list(ph.shape)}")
+            continue
+        if not isinstance(v, Tensor):
+            raise InputMismatch(f"{gf.name}: input {ph.name!r} expects a tensor, got "
+                                f"{type(v).__name__}")
+        if v._symbolic is not None:
+            raise InputMismatch(f"{gf.name}: symbolic tensor passed for {ph.name!r}")
+        if v.dtype is not ph.dtype or len(v.shape) != len(ph.shape) or any(
+                w is not None and h != w for h, w in zip(v.shape, ph.shape)):
+            raise InputMismatch(
+                f"{gf.name}: input {ph.name!r} is {v.dtype.value}{list(v.shape)}, expected "
+                f"{ph.dtype.value}{list(ph.shape)}")
+
+
+# ---------------------------------------------------------------------------
+# native programs
+# ---------------------------------------------------------------------------
+
+_SM_COUNT: Dict[int, int] = {}
+
+
+def _sm_count(dev: int) -> int:
+    n = _SM_COUNT.get(dev)
+    if n is None:
+        import ctypes
+
+        c = ctypes.c_int(0)
+        L = _native.require_device()
+        L.sf_device_info(dev, ctypes.byref(c), None, None, None)
+        n = _SM_COUNT[dev] = max(1, c.value)
+    return n
+
+
+class _NativeSegment:
+    __slots__ = ("plan", "in_roots", "out_roots", "n_launches")
+
+
+class _PySegment:
+    __slots__ = ("op",)
+
+
+class Program:
+    """A graph function lowered for one device and input signature."""
+
+    def __init__(self, gf: GraphFunction, inputs: Sequence, device, libraries, rng_mode: str,
+                 fuse_enabled: bool):
+        self.gf = gf
+        self.device = device
+        self.dev = ordinal_of(device)
+        self.keep: List = []  # constant tensors whose buffers plans point at
+        lw = Lowerer(self.dev, rng_mode)
+        self.in_vals: List[LV] = []
+        for i, (ph, v) in enumerate(zip(gf.inputs, inputs)):
+            lv = lw.new(v.dtype, v.shape, "var" if ph.is_variable_ref else "input")
+            lv.index = i
+            self.in_vals.append(lv)
+        self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)
+        units = fuse(lw.ops, fuse_enabled)
+        self.segments = self._segment(units)
+        self.n_launches = sum(s.n_launches for s in self.segments
+                              if isinstance(s, _NativeSegment))
+
+    # -- construction -------------------------------------------------------------
+    def _segment(self, units) -> list:
+        # last unit index at which each root is used (graph outputs count as "after all")
+        last_use: Dict[int, int] = {}
+        end = len(units)
+        for u, unit in enumerate(units):
+            for op in (unit.ops if isinstance(unit, FusedGroup) else [unit]):
+                for x in op.ins:
+                    last_use[id(x.root())] = max(last_use.get(id(x.root()), -1), u)
+        for v in self.out_vals:
+            last_use[id(v.root())] = end
+        produced_in: Dict[int, int] = {}
+        for u, unit in enumerate(units):
+            for op in (unit.ops if isinstance(unit, FusedGroup) else [unit]):
+                for o in op.outs:
+                    produced_in[id(o)] = u
+
+        segs: list = []
+        run: list = []
+        run_start = 0
+
+        def flush(upto: int):
+            if run:
+                segs.append(self._build_native(run, run_start, upto, last_use, produced_in))
+
+        for u, unit in enumerate(units):
+            if isinstance(unit, LOp) and unit.kind == "py":
+                flush(u)
+                run = []
+                s = _PySegment()
+                s.op = unit
+                segs.append(s)
+                run_start = u + 1
+            else:
+                if not run:
+                    run_start = u
+                run.append(unit)
+        flush(len(units))
+        return segs
+
+    def _build_native(self, units, start, stop, last_use, produced_in) -> _NativeSegment:
+        pw = PlanWriter()
+        slot_of: Dict[int, int] = {}
+        in_roots: List[LV] = []
+        out_roots: List[LV] = []
+        seg_range = range(start, stop)
+
+        def needed_outside(root: LV) -> bool:
+            return last_use.get(id(root), -1) >= stop
+
+        def slot_for_use(x: LV) -> int:
+            r = x.root()
+            s = slot_of.get(id(r))
+            if s is not None:
+                return s
+            if r.kind == "const":
+                t = r.tensor
+                self.keep.append(t)
+                s = pw.slot(SLOT_CONST, r.dtype, r.nbytes, const_ptr=t._ptr() if r.numel else 0)
+            else:
+                # defined outside this segment: an input of the plan
+                s = pw.slot(SLOT_INPUT, r.dtype, r.nbytes, index=len(in_roots))
+                in_roots.append(r)
+            slot_of[id(r)] = s
+            return s
+
+        def slot_for_def(o: LV) -> int:
+            s = slot_of.get(id(o))
+            if s is None:
+                if needed_outside(o):
+                    s = pw.slot(SLOT_OUTPUT, o.dtype, o.nbytes, index=len(out_roots))
+                    out_roots.append(o)
+                else:
+                    s = pw.slot(SLOT_TEMP, o.dtype, o.nbytes)
+                slot_of[id(o)] = s
+            return s
+
+        n_launch = 0
+        for u_off, unit in enumerate(units):
+            u = start + u_off
+            if isinstance(unit, FusedGroup):
+                needed = set()
+                for op in unit.ops:
+                    o = op.outs[0]
+                    if last_use.get(id(o), -1) > u:
+                        needed.add(id(o))
+                n_launch += self._emit_group(pw, unit, needed, slot_for_use, slot_for_def)
+            else:
+                n_launch += self._emit_op(pw, unit, slot_for_use, slot_for_def)
+        pw.n_inputs = len(in_roots)
+        pw.n_outputs = len(out_roots)
+        seg = _NativeSegment()
+        seg.plan = _native.NativePlan(self.dev, pw.serialize(), len(in_roots), len(out_roots))
+        seg.in_roots = in_roots
+        seg.out_roots = out_roots
+        seg.n_launches = n_launch
+        return seg
+
+    def _emit_group(self, pw, group: FusedGroup, needed, use, define) -> int:
+        if len(group.ops) == 1:
+            return self._emit_single_ew(pw, group.ops[0], use, define)
+        name, src, ext, outs = generate_group(group, needed)
+        if not outs:
+            return 0
+        kernel = _native.jit_compile(name, src)
+        in_slots = [use(r) for r in ext]
+        out_slots = [define(o) for o in outs]
+        n = dtypes.element_count(group.shape)
+        grid = max(1, min((n + 255) // 256, _sm_count(self.dev) * 16))
+        ptrs = in_slots + out_slots
+        payload = struct.pack("<QIIII", kernel, grid, 256, 0, len(ptrs))
+        payload += struct.pack("<%di" % len(ptrs), *ptrs)
+        payload += struct.pack("<Iq", 8, n)
+        pw.step(1, payload, defs=out_slots, uses=in_slots)
+        return 1
+
+    def _emit_single_ew(self, pw, op: LOp, use, define) -> int:
+        o = op.outs[0]
+        in_slots, in_shapes, imms = [], [], []
+        for x in op.ins:
+            r = x.root()
+            if r.kind == "const" and r.imm is not None:
+                in_slots.append(-1)
+                imms.append(float(r.imm))
+                in_shapes.append(None)
+            else:
+                in_slots.append(use(x))
+                imms.append(0.0)
+                in_shapes.append(x.shape)
+        name = op.name
+        if name.startswith("cast_"):
+            # casts lower to the cast kernel
+            src = op.ins[0]
+            if in_slots[0] < 0:
+                raise KernelError("cast of an immediate should have been folded")
+            out = define(o)
+            pw.step(11, struct.pack("<iiiiq", src.dtype.tag, o.dtype.tag, in_slots[0], out, o.numel),
+                    defs=[out], uses=[in_slots[0]])
+            return 1
+        opcode = _native.OP[name]
+        in_dtype = op.ins[0].dtype if name != "select" else op.ins[1].dtype
+        out = define(o)
+        pw.step(8, pack_ew_step(opcode, in_dtype, o.shape, in_slots, in_shapes, imms, out),
+                defs=[out], uses=[s for s in in_slots if s >= 0])
+        return 1
+
+    def _emit_op(self, pw, op: LOp, use, define) -> int:
+        k = op.kind
+        if k == "matmul":
+            a, b = op.ins
+            o = op.outs[0]
+            sa, sb = use(a), use(b)
+            so = define(o)
+            m, n = o.shape
+            kk = a.shape[0] if op.attrs["ta"] else a.shape[1]
+            pw.step(2, struct.pack("<iiiiiiqqq", o.dtype.tag, op.attrs["ta"], op.attrs["tb"], sa, sb,
+                                   so, m, n, kk), defs=[so], uses=[sa, sb])
+            return 1
+        if k == "reduce":
+            x = op.ins[0]
+            o = op.outs[0]
+            sx = use(x)
+            so = define(o)
+            mask = 0
+            for ax in op.attrs["axes"]:
+                mask |= 1 << ax
+            shape = list(x.shape) + [1] * (8 - len(x.shape))
+            pw.step(3, struct.pack("<iiiIii8q", 1 if op.name == "reduce_mean" else 0, x.dtype.tag,
+                                   len(x.shape), mask, sx, so, *shape), defs=[so], uses=[sx])
+            return 1
+        if k == "transpose":
+            x = op.ins[0]
+            o = op.outs[0]
+            sx = use(x)
+            so = define(o)
+            if len(x.shape) == 2:
+                pw.step(4, struct.pack("<iiiiqq", x.dtype.tag, sx, so, 0, x.shape[0], x.shape[1]),
+                        defs=[so], uses=[sx])
+            else:
+                from .kernels import _contiguous_strides
+
+                strides = list(reversed(_contiguous_strides(x.shape)))
+                pw.step(8, pack_ew_step(_native.OP["identity"], x.dtype, o.shape, [sx], [strides],
+                                        [0.0], so), defs=[so], uses=[sx])
+            return 1
+        if k == "eye":
+            o = op.outs[0]
+            so = define(o)
+            pw.step(6, struct.pack("<iiq", o.dtype.tag, so, o.shape[0]), defs=[so])
+            return 1
+        if k == "rng":
+            o = op.outs[0]
+            so = define(o)
+            pw.step(9, struct.pack("<iiiiq", op.attrs["kind"], o.dtype.tag, so, 0, o.numel),
+                    defs=[so])
+            return 1
+        if k == "dropout":
+            x = op.ins[0]
+            sx = use(x)
+            so, sm = define(op.outs[0]), define(op.outs[1])
+            pw.step(10, struct.pack("<iiiiqd", x.dtype.tag, sx, so, sm, x.numel, op.attrs["rate"]),
+                    defs=[so, sm], uses=[sx])
+            return 1
+        if k == "var_read":
+            v = op.ins[0]
+            sv = use(v)
+            so = define(op.outs[0])
+            pw.step(7, struct.pack("<iiq", sv, so, v.nbytes), defs=[so], uses=[sv])
+            return 0
+        if k == "var_assign":
+            v, x = op.ins
+            sv = use(v)
+            if x.root().kind == "const" and x.root().imm is not None and v.numel > 0:
+                pw.step(5, struct.pack("<iiqd", v.dtype.tag, sv, v.numel, float(x.root().imm)),
+                        uses=[sv])
+                return 1
+            sx = use(x)
+            pw.step(7, struct.pack("<iiq", sx, sv, v.nbytes), uses=[sx, sv])
+            return 0
+        if k == "var_add":
+            v, x = op.ins
+            sv = use(v)
+            r = x.root()
+            if r.kind == "const" and r.imm is not None:
+                slots, shapes, imms = [sv, -1], [v.shape, None], [0.0, float(r.imm)]
+            else:
+                slots, shapes, imms = [sv, use(x)], [v.shape, x.shape], [0.0, 0.0]
+            pw.step(8, pack_ew_step(_native.OP["add"], v.dtype, v.shape, slots, shapes, imms, sv),
+                    uses=[s for s in slots if s >= 0])
+            return 1
+        raise KernelError(f"lowering: unsupported op kind {k}")
+
+    # -- execution -----------------------------------------------------------------
+    def run(self, inputs: Sequence, libraries) -> List[Tensor]:
+        env: Dict[int, object] = {}
+        for lv, v in zip(self.in_vals, inputs):
+            env[id(lv)] = v
+        device = self.device
+        for seg in self.segments:
+            if isinstance(seg, _NativeSegment):
+                ptrs = [self._ptr_of(env, r) for r in seg.in_roots]
+                outs = seg.plan.run(ptrs)
+                dev = self.dev
+                for r, p in zip(seg.out_roots, outs):
+                    env[id(r)] = _native.DeviceBuffer(dev, p, r.nbytes)
+            else:
+                self._run_py(seg.op, env, libraries)
+        return [self._tensor_of(env, lv) for lv in self.out_vals]
+
+    @staticmethod
+    def _ptr_of(env, root: LV) -> int:
+        h = env[id(root)]
+        if isinstance(h, _native.DeviceBuffer):
+            return h.ptr
+        if isinstance(h, Tensor):
+            return h._ptr()
+        return h._storage_ptr()  # Variable
+
+    def _tensor_of(self, env, lv: LV) -> Tensor:
+        r = lv.root()
+        if r.kind == "const":
+            t = r.tensor
+            host = t._host.reshape(lv.shape) if t._host is not None else None
+            if t._buf is None and host is None:
+                t._device_buffer()
+            return Tensor._adopt(lv.dtype, lv.shape, self.device, t._buf, host)
+        h = env[id(r)]
+        if isinstance(h, _native.DeviceBuffer):
+            return Tensor._adopt(lv.dtype, lv.shape, self.device, h)
+        if isinstance(h, Tensor):
+            host = h._host.reshape(lv.shape) if h._host is not None else None
+            return Tensor._adopt(lv.dtype, lv.shape, self.device, h._buf, host)
+        return h  # Variable (only as an input of a py op)
+
+    def _run_py(self, op: LOp, env, libraries) -> None:
+        ins = [self._tensor_of(env, x) for x in op.ins]
+        kenv = KernelEnv(device=self.device, libraries=tuple(libraries), nested=True)
+        try:
+            outs = op.op_def.kernel(op.attrs, ins, kenv)
+        except _PASSTHROUGH:
+            raise
+        except StageflowError as e:
+            raise KernelError(f"node {op.node_idx} ({op.name}): {e}") from e
+        except Exception as e:
+            raise KernelError(f"node {op.node_idx} ({op.name}): {e}") from e
+        for lv, t in zip(op.outs, outs):
+            env[id(lv)] = t
+
+
+def _signature(inputs: Sequence) -> Tuple:
+    return tuple((type(v).__name__ == "Variable", v.dtype, v.shape) for v in inputs)
+
+
+def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
+    cache = gf._plan
+    if cache is None:
+        cache = gf._plan = {}
+    key = (device, _signature(inputs))
+    prog = cache.get(key)
+    if prog is None:
+        opts = get_runtime().options
+        prog = Program(gf, inputs, device, libraries, opts.rng, opts.fuse)
+        cache[key] = prog
+    return prog
+
+
+def _needs_interpretation(gf: GraphFunction, inputs, device, rt) -> bool:
+    if len(rt.devices) == 1:
+        return False
+    if any(n.device is not None and n.device != device for n in gf.nodes):
+        return True
+    return any(isinstance(v, Tensor) and v.device != device for v in inputs)
+
+
+def execute_graph(gf: GraphFunction, inputs: Sequence, env: Optional[KernelEnv] = None,
+                  workers: Optional[int] = None) -> List[Tensor]:
+    rt = get_runtime()
+    _bind_inputs(gf, inputs)
+    if env is not None:
+        device = env.device
+        libraries = (gf.library,) + tuple(env.libraries)
+    else:
+        device = current_context().scope_device() or rt.devices[0].name
+        libraries = (gf.library,)
+    if _needs_interpretation(gf, inputs, device, rt):
+        return _interpret(gf, inputs, device, libraries)
+    prog = _program_for(gf, inputs, device, libraries[1:])
+    rt.stats.count_graph_launch()
+    return prog.run(inputs, libraries)
+
+
+def _interpret(gf: GraphFunction, inputs, device, libraries) -> List[Tensor]:
+    """Per-node launches with the reference's transparent-copy accounting."""
+    rt = get_runtime()
+    n_in = len(gf.inputs)
+    vals: Dict[Tuple[int, int], object] = {(i, 0): v for i, v in enumerate(inputs)}
+    for j, node in enumerate(gf.nodes):
+        vid = n_in + j
+        if node.op == "constant":
+            vals[(vid, 0)] = node.attrs["value"]
+            continue
+        from .ops import get_op_def
+
+        target = node.device or device
+        kenv = KernelEnv(device=target, libraries=libraries, nested=True)
+        ins, moved = [], {}
+        for r in node.inputs:
+            v = vals[r]
+            if isinstance(v, Tensor) and v.device != target:
+                c = moved.get(id(v))
+                if c is None:
+                    c = moved[id(v)] = relabel(v, target)
+                    rt.stats.count_copy()
+                v = c
+            ins.append(v)
+        try:
+            outs = get_op_def(node.op).kernel(node.attrs, ins, kenv)
+        except _PASSTHROUGH:
+            raise
+        except Exception as e:
+            raise KernelError(f"node {j} ({node.op}): {e}") from e
+        for k, o in enumerate(outs):
+            vals[(vid, k)] = o
+    return [vals[ref] for _, ref in gf.outputs]
+
+
+def execute(gf: GraphFunction, inputs: Sequence, captured: Sequence = (),
+            workers: Optional[int] = None) -> List[Tensor]:
+    """Run a graph function directly (inputs, then captured values)."""
+    everything = list(inputs) + list(captured)
+    rt = get_runtime()
+    device = current_context().scope_device()
+    if device is None:
+        device = next((v.device for v in everything if isinstance(v, Tensor)), rt.devices[0].name)
+    return execute_graph(gf, everything, env=KernelEnv(device=device), workers=workers)
+
+
+def run_node_for_folding(node: Node, inputs: Sequence[Tensor], library) -> List[Tensor]:
+    """Evaluate one stateless node on constant inputs with the GPU kernels."""
+    from .ops import get_op_def
+
+    rt = get_runtime()
+    env = KernelEnv(device=rt.devices[0].name, libraries=(library,), nested=True)
+    try:
+        return get_op_def(node.op).kernel(node.attrs, list(inputs), env)
+    except StageflowError:
+        raise
+    except Exception as e:
+        raise KernelError(f"folding {node.op}: {e}") from e

@@ -1,0 +1,494 @@
+"""Lowering of graph functions to native programs (the staged executor's compiler).
+
+Replaces the reference's per-node interpreter (stageflow/executor.py:58-269).
+A GraphFunction is compiled once per (device, concrete input signature):
+
+1. *Flatten*: nodes become lowered ops over lowered values (``LV``).
+   ``call_function`` callees are inlined; ``reshape``/``identity`` become
+   aliases (no data movement); ``constant`` becomes a plan-owned buffer or,
+   when it is one element or a splat, an immediate literal.
+2. *Fuse*: maximal runs of elementwise/broadcast ops over one iteration
+   shape become a single generated CUDA kernel (registers only, one load per
+   external input element, one store per value needed outside the group),
+   compiled for sm_100a by NVRTC against the same ``sf_ops.cuh`` the eager
+   kernels use — hence bit-identical results.
+3. *Segment*: ops the native executor cannot run (host callbacks, cond /
+   while predicates, plugin ops without a lowering, host-RNG parity draws)
+   split the program; everything between them is one native plan executed
+   by a single ``sf_plan_run`` call (csrc/sf_plan.cpp), with temporaries
+   allocated at their defining step and freed after their last use.
+"""
+from __future__ import annotations
+
+import hashlib
+import struct
+from typing import Any, Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native, dtypes
+from .dtypes import DType
+from .errors import KernelError, MissingFunction
+from .tensor import Tensor
+
+# ---------------------------------------------------------------------------
+# lowered values and ops
+# ---------------------------------------------------------------------------
+
+
+class LV:
+    """A lowered value.  kinds: input, var, const, op, alias."""
+
+    __slots__ = ("id", "dtype", "shape", "kind", "index", "tensor", "base", "imm", "producer")
+
+    def __init__(self, id_, dtype: DType, shape, kind: str):
+        self.id = id_
+        self.dtype = dtype
+        self.shape = tuple(shape)
+        self.kind = kind
+        self.index = -1       # input ordinal
+        self.tensor = None    # const value
+        self.base = None      # alias target
+        self.imm = None       # scalar literal if the value is a known splat
+        self.producer = None  # LOp
+
+    @property
+    def numel(self) -> int:
+        return dtypes.element_count(self.shape)
+
+    @property
+    def nbytes(self) -> int:
+        return self.numel * self.dtype.width
+
+    def root(self) -> "LV":
+        v = self
+        while v.kind == "alias":
+            v = v.base
+        return v
+
+
+class LOp:
+    __slots__ = ("kind", "name", "ins", "outs", "attrs", "node_idx", "op_def")
+
+    def __init__(self, kind, name, ins, outs, attrs=None, node_idx=-1, op_def=None):
+        self.kind = kind      # ew | matmul | reduce | transpose | eye | rng | dropout |
+        self.name = name      # var_read | var_assign | var_add | py
+        self.ins = ins
+        self.outs = outs
+        self.attrs = attrs or {}
+        self.node_idx = node_idx
+        self.op_def = op_def
+
+
+# elementwise ops the fuser understands: name -> (arity, result dtype rule)
+_EW_BUILTIN = {
+    "add": 2, "sub": 2, "mul": 2, "div": 2, "neg": 1, "exp": 1, "log": 1, "softplus": 1,
+    "relu": 1, "step_positive": 1, "greater": 2,
+}
+
+
+class Lowerer:
+    def __init__(self, device_ordinal: int, rng_mode: str):
+        self.dev = device_ordinal
+        self.rng_mode = rng_mode
+        self.values: List[LV] = []
+        self.ops: List[LOp] = []
+        self.inputs: List[LV] = []
+
+    def new(self, dtype, shape, kind) -> LV:
+        v = LV(len(self.values), dtype, shape, kind)
+        self.values.append(v)
+        return v
+
+    # -- graph flattening -------------------------------------------------------
+    def lower_graph(self, gf, in_vals: Sequence[LV], libraries) -> List[LV]:
+        from .ops import get_op_def
+
+        libs = (gf.library,) + tuple(libraries)
+        n_in = len(gf.inputs)
+        env: Dict[Tuple[int, int], LV] = {}
+        for i, v in enumerate(in_vals):
+            env[(i, 0)] = v
+        for j, node in enumerate(gf.nodes):
+            ins = [env[r] for r in node.inputs]
+            outs = self.lower_node(node, j, ins, libs, get_op_def(node.op))
+            for k, o in enumerate(outs):
+                env[(n_in + j, k)] = o
+        return [env[ref] for _, ref in gf.outputs]
+
+    def _out(self, node, k=0) -> LV:
+        dt, shape = node.out_specs[k]
+        return self.new(dt, shape, "op")
+
+    def emit(self, kind, name, ins, outs, node_idx, attrs=None, op_def=None) -> List[LV]:
+        op = LOp(kind, name, ins, outs, attrs, node_idx, op_def)
+        for o in outs:
+            o.producer = op
+        self.ops.append(op)
+        return outs
+
+    def lower_node(self, node, j, ins: List[LV], libs, op_def) -> List[LV]:
+        op = node.op
+        if op == "constant":
+            t: Tensor = node.attrs["value"]
+            v = self.new(t.dtype, t.shape, "const")
+            v.tensor = t
+            v.imm = _splat_value(t)
+            return [v]
+        if op in ("reshape", "identity"):
+            dt, shape = node.out_specs[0]
+            v = self.new(dt, _concrete(shape, ins[0].shape if op == "identity" else None), "alias")
+            v.base = ins[0]
+            v.imm = ins[0].imm if ins[0].kind in ("const", "alias") else None
+            if v.imm is None and ins[0].root().kind == "const":
+                v.imm = ins[0].root().imm
+            return [v]
+        if op in _EW_BUILTIN:
+            return self.emit("ew", op, ins, [self._shaped_out(node, ins)], j)
+        if op == "broadcast_to":
+            return self.emit("ew", "identity", ins, [self._shaped_out(node, ins)], j)
+        if op == "matmul":
+            a, b = ins
+            out = self.new(a.dtype, (a.shape[0], b.shape[1]), "op")
+            return self.emit("matmul", op, ins, [out], j, {"ta": 0, "tb": 0})
+        if op == "transpose":
+            x = ins[0]
+            out = self.new(x.dtype, tuple(reversed(x.shape)), "op")
+            return self.emit("transpose", op, ins, [out], j)
+        if op in ("reduce_sum", "reduce_mean"):
+            from .kernels import normalize_axes, reduced_shape
+
+            x = ins[0]
+            if x.dtype is DType.boolean or (op == "reduce_mean" and x.dtype is DType.int32):
+                return self._py(node, j, ins, op_def)
+            axes = normalize_axes(op, len(x.shape), node.attrs.get("axes"))
+            shape = reduced_shape(op, x.shape, node.attrs.get("axes"),
+                                  node.attrs.get("keepdims", False))
+            out = self.new(x.dtype, shape, "op")
+            return self.emit("reduce", op, ins, [out], j, {"axes": axes})
+        if op == "eye":
+            dt = node.attrs["dtype"]
+            n = node.attrs["size"]
+            return self.emit("eye", op, [], [self.new(dt, (n, n), "op")], j)
+        if op == "random_normal" and self.rng_mode == "device":
+            dt = node.attrs["dtype"]
+            return self.emit("rng", op, [], [self.new(dt, tuple(node.attrs["shape"]), "op")], j,
+                             {"kind": 0})
+        if op == "dropout" and self.rng_mode == "device":
+            x = ins[0]
+            outs = [self.new(x.dtype, x.shape, "op"), self.new(x.dtype, x.shape, "op")]
+            return self.emit("dropout", op, ins, outs, j, {"rate": node.attrs["rate"]})
+        if op == "read_variable":
+            v = ins[0]
+            return self.emit("var_read", op, ins, [self.new(v.dtype, v.shape, "op")], j)
+        if op == "assign_variable":
+            return self.emit("var_assign", op, ins, [], j)
+        if op == "assign_add_variable":
+            return self.emit("var_add", op, ins, [], j)
+        if op == "call_function":
+            callee = _resolve(node.attrs["function"], libs)
+            outs = self.lower_graph(callee, ins, libs)
+            return outs
+        low = getattr(op_def, "lowering", None)
+        if low is not None:
+            kind = low[0]
+            if kind == "ew":
+                return self.emit("ew", low[1], ins, [self._shaped_out(node, ins)], j)
+            if kind == "cast":
+                return self.emit("ew", "cast_" + node.out_specs[0][0].value, ins,
+                                 [self._shaped_out(node, ins)], j)
+            if kind == "rng" and self.rng_mode == "device":
+                dt = node.attrs["dtype"]
+                return self.emit("rng", op, [], [self.new(dt, tuple(node.attrs["shape"]), "op")],
+                                 j, {"kind": low[1]})
+        return self._py(node, j, ins, op_def)
+
+    def _shaped_out(self, node, ins) -> LV:
+        dt, shape = node.out_specs[0]
+        if None in tuple(shape):
+            shape = ins[0].shape
+            for x in ins[1:]:
+                shape = dtypes.broadcast_shapes(shape, x.shape)
+        return self.new(dt, shape, "op")
+
+    def _py(self, node, j, ins, op_def) -> List[LV]:
+        outs = [self.new(dt, shape, "op") for dt, shape in node.out_specs]
+        return self.emit("py", node.op, ins, outs, j, dict(node.attrs), op_def)
+
+
+def _concrete(shape, fallback):
+    if None in tuple(shape):
+        if fallback is None:
+            raise KernelError("lowering needs concrete shapes")
+        return fallback
+    return shape
+
+
+def _resolve(name_or_fn, libs):
+    from .graph import GraphFunction
+
+    if isinstance(name_or_fn, GraphFunction):
+        return name_or_fn
+    for lib in libs:
+        f = lib.get(name_or_fn)
+        if f is not None:
+            return f
+    raise MissingFunction(f"no graph function named {name_or_fn!r} in scope")
+
+
+def _splat_value(t: Tensor):
+    """The single value of a constant whose elements are all equal (or None)."""
+    if t.size == 0:
+        return None
+    if t.size == 1:
+        h = t._host if t._host is not None else t.raw()
+        return h.reshape(-1)[0].item()
+    if t.size > (1 << 22):
+        return None
+    h = t.raw().reshape(-1)
+    first = h[0]
+    if t.dtype.is_float:
+        # bitwise comparison (distinguishes -0.0 and NaN payloads)
+        view = h.view(np.uint32 if t.dtype is DType.float32 else np.uint64)
+        if np.all(view == view[0]):
+            return first.item()
+        return None
+    return first.item() if np.all(h == first) else None
+
+
+# ---------------------------------------------------------------------------
+# fusion of elementwise runs
+# ---------------------------------------------------------------------------
+
+
+class FusedGroup:
+    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs")
+
+    def __init__(self, shape):
+        self.ops: List[LOp] = []
+        self.shape = shape
+        self.outs_needed: List[LV] = []
+        self.ext_inputs: List[LV] = []
+
+
+def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
+    """Group consecutive elementwise ops sharing one output shape."""
+    units: List[Any] = []
+    cur: Optional[FusedGroup] = None
+    for op in ops:
+        if op.kind == "ew" and fuse_enabled:
+            shape = op.outs[0].shape
+            if cur is not None and cur.shape == shape:
+                cur.ops.append(op)
+                continue
+            cur = FusedGroup(shape)
+            cur.ops.append(op)
+            units.append(cur)
+            continue
+        cur = None
+        units.append(op)
+    return units
+
+
+# ---------------------------------------------------------------------------
+# code generation
+# ---------------------------------------------------------------------------
+
+_CTYPE = {DType.float32: "float", DType.float64: "double", DType.int32: "int",
+          DType.boolean: "bool"}
+
+_UNARY_FN = {
+    "neg": "sf::neg", "exp": "sf::exp_", "log": "sf::log_", "softplus": "sf::softplus",
+    "relu": "sf::relu", "step_positive": "sf::step_pos", "tanh": "sf::tanh_",
+    "sqrt": "sf::sqrt_", "rsqrt": "sf::rsqrt_", "sigmoid": "sf::sigmoid", "abs": "sf::abs_",
+    "square": "sf::square", "reciprocal": "sf::recip", "cos": "sf::cos_", "sin": "sf::sin_",
+}
+_BINARY_FN = {"add": "sf::add", "sub": "sf::sub", "mul": "sf::mul", "div": "sf::div",
+              "maximum": "sf::maximum", "minimum": "sf::minimum"}
+_COMPARE = {"greater": ">", "less": "<", "equal": "==", "greater_equal": ">="}
+
+
+def c_literal(value, dtype: DType) -> str:
+    if dtype is DType.float32:
+        bits = struct.unpack("<I", struct.pack("<f", float(value)))[0]
+        return f"__int_as_float(0x{bits:08x})"
+    if dtype is DType.float64:
+        bits = struct.unpack("<Q", struct.pack("<d", float(value)))[0]
+        return f"__longlong_as_double(0x{bits:016x}ll)"
+    if dtype is DType.int32:
+        v = int(value)
+        return f"(int){v}" if v != -(2 ** 31) else "(int)(-2147483647 - 1)"
+    return "true" if value else "false"
+
+
+def _strides_for(src_shape, out_shape):
+    nd = len(out_shape)
+    cs, acc = [], 1
+    for d in reversed(src_shape):
+        cs.append(acc)
+        acc *= d
+    cs = cs[::-1]
+    pad = nd - len(src_shape)
+    return [0] * pad + [0 if src_shape[i] == 1 else cs[i] for i in range(len(src_shape))]
+
+
+def _index_expr(src_shape, out_shape, idx: str) -> str:
+    """C expression for the flat offset of the broadcast source at flat index idx."""
+    if tuple(src_shape) == tuple(out_shape):
+        return idx
+    if dtypes.element_count(src_shape) == 1:
+        return "0"
+    strides = _strides_for(src_shape, out_shape)
+    terms = []
+    inner = 1
+    for d in range(len(out_shape) - 1, -1, -1):
+        ext = out_shape[d]
+        st = strides[d]
+        if st and ext != 1:
+            coord = f"({idx} / {inner})" if inner != 1 else idx
+            if d != 0:
+                coord = f"({coord} % {ext})"
+            terms.append(f"{coord} * {st}" if st != 1 else coord)
+        inner *= ext
+    return " + ".join(terms) if terms else "0"
+
+
+def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List[LV], List[LV]]:
+    """CUDA source for a fused group. Returns (name, source, in_values, out_values)."""
+    shape = group.shape
+    n = dtypes.element_count(shape)
+    produced = {id(o) for op in group.ops for o in op.outs}
+    # external inputs: (view as consumed, storage root); an alias (reshape)
+    # is loaded with its own shape over the root's buffer
+    ext: List[Tuple[LV, LV]] = []
+    names: Dict[Tuple[int, tuple], str] = {}
+    for op in group.ops:
+        for x in op.ins:
+            r = x.root()
+            if id(r) in produced:
+                continue
+            if r.kind == "const" and r.imm is not None:
+                continue
+            key = (id(r), x.shape)
+            if key not in names:
+                names[key] = f"in{len(ext)}"
+                ext.append((x, r))
+    outs = [op.outs[0] for op in group.ops if id(op.outs[0]) in needed_after]
+    idx_t = "long long" if n >= (1 << 31) else "int"
+    lines = []
+    for k, (x, r) in enumerate(ext):
+        ct = _CTYPE[r.dtype]
+        lines.append(f"    const {ct} in{k} = ((const {ct}*)a.p[{k}])"
+                     f"[{_index_expr(x.shape, shape, 'i')}];")
+
+    def ref(x: LV) -> str:
+        r = x.root()
+        nm = names.get((id(r), x.shape)) or names.get((id(r), r.shape))
+        if nm is not None:
+            return nm
+        if r.kind == "const" and r.imm is not None:
+            return c_literal(r.imm, r.dtype)
+        raise KernelError("fusion: unresolved operand")
+
+    for t, op in enumerate(group.ops):
+        o = op.outs[0]
+        ct = _CTYPE[o.dtype]
+        args = [ref(x) for x in op.ins]
+        # operands of a broadcasting op that have a different (smaller) shape
+        # were loaded through broadcast indexing already (ext inputs), and
+        # in-group values always have the group shape.
+        nm = op.name
+        if nm == "identity":
+            expr = args[0]
+        elif nm in _UNARY_FN:
+            expr = f"{_UNARY_FN[nm]}({args[0]})"
+        elif nm in _BINARY_FN:
+            expr = f"{_BINARY_FN[nm]}({args[0]}, {args[1]})"
+        elif nm in _COMPARE:
+            expr = f"({args[0]} {_COMPARE[nm]} {args[1]})"
+        elif nm == "isfinite":
+            expr = f"sf::isfinite_({args[0]})"
+        elif nm == "logical_not":
+            expr = f"(!{args[0]})"
+        elif nm == "select":
+            expr = f"({args[0]} ? {args[1]} : {args[2]})"
+        elif nm.startswith("cast_"):
+            expr = f"({ct})({args[0]})"
+        else:
+            raise KernelError(f"fusion: no code for elementwise op {nm!r}")
+        lines.append(f"    const {ct} v{t} = {expr};")
+        names[(id(o), o.shape)] = f"v{t}"
+    for k, o in enumerate(outs):
+        ct = _CTYPE[o.dtype]
+        lines.append(f"    (({ct}*)a.p[{len(ext) + k}])[i] = {names[(id(o), o.shape)]};")
+    body = "\n".join(lines)
+    n_ptr = len(ext) + len(outs)
+    src_core = (f"struct Params {{ void* p[{max(1, n_ptr)}]; long long n; }};\n"
+                f"extern \"C\" __global__ void __launch_bounds__(256) KNAME(const __grid_constant__ "
+                f"Params a) {{\n"
+                f"  const {idx_t} stride = ({idx_t})gridDim.x * blockDim.x;\n"
+                f"  for ({idx_t} i = ({idx_t})blockIdx.x * blockDim.x + threadIdx.x; i < ({idx_t})a.n;"
+                f" i += stride) {{\n{body}\n  }}\n}}\n")
+    digest = hashlib.sha1(src_core.encode()).hexdigest()[:16]
+    name = f"sf_fused_{digest}"
+    source = '#include "sf_ops.cuh"\n' + src_core.replace("KNAME", name)
+    return name, source, [r for _, r in ext], outs
+
+
+# ---------------------------------------------------------------------------
+# plan serialisation (format documented in csrc/sf_plan.cpp)
+# ---------------------------------------------------------------------------
+
+SLOT_INPUT, SLOT_CONST, SLOT_TEMP, SLOT_OUTPUT = 0, 1, 2, 3
+
+
+class PlanWriter:
+    def __init__(self):
+        self.slots: List[list] = []   # [kind, dtype_tag, index, nbytes, const_ptr, def, last]
+        self.steps: List[Tuple[int, bytes]] = []
+        self.n_inputs = 0
+        self.n_outputs = 0
+
+    def slot(self, kind, dtype: DType, nbytes: int, index=-1, const_ptr=0) -> int:
+        self.slots.append([kind, dtype.tag, index, nbytes, const_ptr, -1, -1])
+        return len(self.slots) - 1
+
+    def step(self, kind: int, payload: bytes, defs=(), uses=()) -> int:
+        s = len(self.steps)
+        self.steps.append((kind, payload))
+        for d in defs:
+            if self.slots[d][5] < 0:
+                self.slots[d][5] = s
+        for u in list(uses) + list(defs):
+            self.slots[u][6] = max(self.slots[u][6], s)
+        return s
+
+    def serialize(self) -> bytes:
+        parts = [struct.pack("<IIiiii", 0x4C504653, 1, len(self.slots), self.n_inputs,
+                             self.n_outputs, len(self.steps))]
+        for kind, tag, index, nbytes, cptr, d, last in self.slots:
+            parts.append(struct.pack("<BBHiQQii", kind, tag, 0, index, max(1, nbytes), cptr, d,
+                                     last))
+        for kind, payload in self.steps:
+            parts.append(struct.pack("<II", kind, len(payload)))
+            parts.append(payload)
+        return b"".join(parts)
+
+
+def pack_ew_step(op: int, dtype: DType, out_shape, in_slots, in_shapes, imms, out_slot) -> bytes:
+    nd = len(out_shape)
+    if nd > _native.MAX_DIMS:
+        raise KernelError("rank exceeds backend limit")
+    shp = list(out_shape) + [1] * (_native.MAX_DIMS - nd)
+    slots = list(in_slots) + [-1] * (3 - len(in_slots))
+    ims = list(imms) + [0.0] * (3 - len(imms))
+    strides = []
+    for j in range(3):
+        if j < len(in_shapes) and in_shapes[j] is not None:
+            st = in_shapes[j] if isinstance(in_shapes[j], list) else _strides_for(in_shapes[j],
+                                                                                  out_shape)
+        else:
+            st = [0] * nd
+        strides.extend(list(st) + [0] * (_native.MAX_DIMS - nd))
+    return struct.pack("<iiii3ii3d8q24q", op, dtype.tag, nd, len(in_slots), *slots, out_slot, *ims,
+                       *shp, *strides)
