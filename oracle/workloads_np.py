@@ -97,6 +97,141 @@ def mlp_losses(batch, iterations, seed=0):
 
 
 # ---------------------------------------------------------------------------
+# L2HMC sampler — builder-defined (paper_1903_01855_b200/workloads/l2hmc.py)
+# ---------------------------------------------------------------------------
+
+class L2HMC:
+    """NumPy restatement of workloads/l2hmc.py op for op, in float32.
+
+    Random draws follow the reference runtime's host stream
+    (``default_rng(runtime_seed)``): per transition standard_normal((B,2))
+    for the forward and the backward kernels, then random((B,)) for the
+    direction and random((B,)) for the accept test.
+    """
+
+    X_DIM, N_HIDDEN, N_STEPS, EPS = 2, 10, 10, 0.1
+
+    def __init__(self, batch, seed=0, runtime_seed=0, x0=None):
+        import math
+
+        rng = np.random.default_rng(seed)
+        self.batch = batch
+
+        def dense(n_in, n_out, f):
+            w = (rng.standard_normal((n_in, n_out)) * math.sqrt(2.0 * f / n_in)).astype(F32)
+            return w, np.zeros((1, n_out), dtype=F32)
+
+        def net(factor):
+            return dict(v=dense(2, 10, 1 / 3), x=dense(2, 10, factor / 3), t=dense(2, 10, 1 / 3),
+                        h=dense(10, 10, 1.0), scale=dense(10, 2, 0.001), transl=dense(10, 2, 0.001),
+                        transf=dense(10, 2, 0.001), cs=np.zeros((1, 2), F32),
+                        ct=np.zeros((1, 2), F32))
+
+        self.pos_net = net(2.0)
+        self.mom_net = net(1.0)
+        sigma = np.array([[50.05, -49.95], [-49.95, 50.05]])
+        self.A = np.linalg.inv(sigma).astype(F32)
+        self.ts = [np.array([[math.cos(2 * math.pi * i / 10), math.sin(2 * math.pi * i / 10)]],
+                            dtype=F32) for i in range(10)]
+        self.masks = []
+        for _ in range(10):
+            idx = rng.permutation(2)[:1]
+            m = np.zeros((1, 2))
+            m[0, idx] = 1.0
+            self.masks.append((m.astype(F32), (1.0 - m).astype(F32)))
+        x = rng.standard_normal((batch, 2)).astype(F32)
+        self.x = x if x0 is None else np.asarray(x0, dtype=F32)
+        self.rt = np.random.default_rng(runtime_seed)
+
+    @staticmethod
+    def _dense(layer, x):
+        w, b = layer
+        return np.matmul(x, w) + b
+
+    def _net(self, n, v, x, t):
+        h = (self._dense(n["v"], v) + self._dense(n["x"], x)) + self._dense(n["t"], t)
+        h = np.maximum(h, 0).astype(F32)
+        h = np.maximum(self._dense(n["h"], h), 0).astype(F32)
+        scale = np.tanh(self._dense(n["scale"], h)) * np.exp(n["cs"])
+        transl = self._dense(n["transl"], h)
+        transf = np.tanh(self._dense(n["transf"], h)) * np.exp(n["ct"])
+        return scale, transl, transf
+
+    def potential(self, x):
+        return np.sum(np.matmul(x, self.A) * x, axis=1).astype(F32) * F32(0.5)
+
+    def grad_potential(self, x):
+        g = np.full(x.shape, F32(1.0) * F32(0.5), dtype=F32)
+        xa = np.matmul(x, self.A)
+        return np.add(g * xa, np.matmul(g * x, np.ascontiguousarray(self.A.T)))
+
+    def hamiltonian(self, x, v):
+        return self.potential(x) + np.sum(v * v, axis=1).astype(F32) * F32(0.5)
+
+    def _mom(self, x, v, t, fwd):
+        e = F32(self.EPS)
+        grad = self.grad_potential(x)
+        scale, transl, transf = self._net(self.mom_net, x, grad, t)
+        scale = scale * (F32(0.5 * self.EPS) if fwd else F32(-0.5 * self.EPS))
+        transf = transf * e
+        inner = (np.exp(transf) * grad - transl) * F32(0.5 * self.EPS)
+        v = v * np.exp(scale) - inner if fwd else np.exp(scale) * (v + inner)
+        return v, np.sum(scale, axis=1).astype(F32)
+
+    def _pos(self, x, v, t, mask, mask_inv, fwd):
+        e = F32(self.EPS)
+        scale, transl, transf = self._net(self.pos_net, v, mask * x, t)
+        scale = scale * (e if fwd else F32(-self.EPS))
+        transf = transf * e
+        if fwd:
+            moved = x * np.exp(scale) + (np.exp(transf) * v + transl) * e
+            x = mask * x + mask_inv * moved
+        else:
+            back = x - (np.exp(transf) * v + transl) * e
+            x = mask * x + mask_inv * (np.exp(scale) * back)
+        return x, np.sum(mask_inv * scale, axis=1).astype(F32)
+
+    def _lf(self, x, v, i, fwd):
+        j = i if fwd else self.N_STEPS - i - 1
+        t = self.ts[j]
+        m, mi = self.masks[j]
+        v, l1 = self._mom(x, v, t, fwd)
+        if fwd:
+            x, l2 = self._pos(x, v, t, m, mi, True)
+            x, l3 = self._pos(x, v, t, mi, m, True)
+        else:
+            x, l2 = self._pos(x, v, t, mi, m, False)
+            x, l3 = self._pos(x, v, t, m, mi, False)
+        v, l4 = self._mom(x, v, t, fwd)
+        return x, v, (l1 + l2) + (l3 + l4)
+
+    def _kernel(self, x, fwd):
+        v = self.rt.standard_normal((self.batch, 2)).astype(F32)
+        xp, vp, logdet = x, v, None
+        for i in range(self.N_STEPS):
+            xp, vp, ld = self._lf(xp, vp, i, fwd)
+            logdet = ld if logdet is None else logdet + ld
+        delta = (self.hamiltonian(x, v) - self.hamiltonian(xp, vp)) + logdet
+        with np.errstate(over="ignore", invalid="ignore"):
+            prob = np.exp(np.minimum(delta, F32(0.0)))
+        prob = np.where(np.isfinite(prob), prob, F32(0.0)).astype(F32)
+        return xp, prob
+
+    def transition(self):
+        x = self.x
+        b = self.batch
+        xf, pf = self._kernel(x, True)
+        xb, pb = self._kernel(x, False)
+        fwd = (self.rt.random((b,)).astype(F32) > F32(0.5)).astype(F32)
+        bwd = F32(1.0) - fwd
+        x_post = fwd.reshape(b, 1) * xf + bwd.reshape(b, 1) * xb
+        acc_prob = fwd * pf + bwd * pb
+        acc = (acc_prob > self.rt.random((b,)).astype(F32)).astype(F32)
+        self.x = acc.reshape(b, 1) * x_post + (F32(1.0) - acc).reshape(b, 1) * x
+        return np.concatenate([self.x.ravel(), acc_prob.ravel()])
+
+
+# ---------------------------------------------------------------------------
 # C2 microbenchmark — builder-defined (SURVEY.md §8(d) row C2)
 # ---------------------------------------------------------------------------
 

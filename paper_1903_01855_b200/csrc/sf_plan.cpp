@@ -53,6 +53,13 @@ struct Step {
   unsigned grid = 1, block = 1, smem = 0;
   std::vector<int32_t> ptr_slots;
   std::vector<char> scalars;
+  // run-time patches of the scalar blob: kind 0 = device RNG seed,
+  // kind 1 = reserve `count` Philox counters and write the base offset
+  struct Patch {
+    uint32_t kind, offset;
+    uint64_t count;
+  };
+  std::vector<Patch> patches;
   std::vector<int32_t> frees;  // temp slots to release after this step
   std::vector<int32_t> defs;   // temp/output slots to allocate before this step
 };
@@ -113,6 +120,17 @@ static int run_step(Plan* p, Device* d, Step& s, std::vector<void*>& ptr) {
       }
       if (!s.scalars.empty())
         std::memcpy(blob.data() + s.ptr_slots.size() * 8, s.scalars.data(), s.scalars.size());
+      if (!s.patches.empty()) {
+        std::lock_guard<std::mutex> lk(d->rng_mu);
+        for (const auto& pt : s.patches) {
+          uint64_t v = d->rng_seed;
+          if (pt.kind == 1) {
+            v = d->rng_offset;
+            d->rng_offset += pt.count;
+          }
+          std::memcpy(blob.data() + s.ptr_slots.size() * 8 + pt.offset, &v, 8);
+        }
+      }
       return jit_launch(d, s.kernel, s.grid, s.block, s.smem, blob.data(), blob.size());
     }
     case 2:
@@ -235,6 +253,17 @@ int sf_plan_create(int dev, const void* desc, size_t desc_bytes, void** out) {
       off += 4;
       if (off + ns > b.size()) return bad("jit scalars");
       s.scalars.assign(b.begin() + off, b.begin() + off + ns);
+      off += ns;
+      if (off + 4 <= b.size()) {
+        const uint32_t np = at<uint32_t>(b, off);
+        off += 4;
+        for (uint32_t k = 0; k < np; ++k, off += 16) {
+          if (off + 16 > b.size()) return bad("jit patches");
+          Step::Patch pt{at<uint32_t>(b, off), at<uint32_t>(b, off + 4), at<uint64_t>(b, off + 8)};
+          if (pt.offset + 8 > ns) return bad("jit patch offset");
+          s.patches.push_back(pt);
+        }
+      }
     }
     if (s.kind != 7) ++p->n_launches;
   }

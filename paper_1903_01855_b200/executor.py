@@ -82,6 +82,14 @@ def _sm_count(dev: int) -> int:
     return n
 
 
+def _unit_ops(unit):
+    if isinstance(unit, FusedGroup):
+        return unit.ops
+    if isinstance(unit, tuple):  # (RowProgram, planner)
+        return unit[0].ops
+    return [unit]
+
+
 class _NativeSegment:
     __slots__ = ("plan", "in_roots", "out_roots", "n_launches")
 
@@ -106,7 +114,9 @@ class Program:
             lv.index = i
             self.in_vals.append(lv)
         self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)
-        units = fuse(lw.ops, fuse_enabled)
+        from .rowfuse import plan_rows
+
+        units = fuse(plan_rows(lw.ops) if fuse_enabled else lw.ops, fuse_enabled)
         self.segments = self._segment(units)
         self.n_launches = sum(s.n_launches for s in self.segments
                               if isinstance(s, _NativeSegment))
@@ -117,14 +127,14 @@ class Program:
         last_use: Dict[int, int] = {}
         end = len(units)
         for u, unit in enumerate(units):
-            for op in (unit.ops if isinstance(unit, FusedGroup) else [unit]):
+            for op in _unit_ops(unit):
                 for x in op.ins:
                     last_use[id(x.root())] = max(last_use.get(id(x.root()), -1), u)
         for v in self.out_vals:
             last_use[id(v.root())] = end
         produced_in: Dict[int, int] = {}
         for u, unit in enumerate(units):
-            for op in (unit.ops if isinstance(unit, FusedGroup) else [unit]):
+            for op in _unit_ops(unit):
                 for o in op.outs:
                     produced_in[id(o)] = u
 
@@ -191,7 +201,11 @@ class Program:
         n_launch = 0
         for u_off, unit in enumerate(units):
             u = start + u_off
-            if isinstance(unit, FusedGroup):
+            if isinstance(unit, tuple):
+                needed = {id(o) for op in unit[0].ops for o in op.outs
+                          if last_use.get(id(o), -1) > u}
+                n_launch += self._emit_rows(pw, unit, needed, slot_for_use, slot_for_def)
+            elif isinstance(unit, FusedGroup):
                 needed = set()
                 for op in unit.ops:
                     o = op.outs[0]
@@ -224,6 +238,31 @@ class Program:
         payload = struct.pack("<QIIII", kernel, grid, 256, 0, len(ptrs))
         payload += struct.pack("<%di" % len(ptrs), *ptrs)
         payload += struct.pack("<Iq", 8, n)
+        pw.step(1, payload, defs=out_slots, uses=in_slots)
+        return 1
+
+    def _emit_rows(self, pw, unit, needed, use, define) -> int:
+        from .rowfuse import generate_rowprog
+
+        rp, planner = unit
+        name, src, ext, outs, rng_counts, _n_ptr = generate_rowprog(rp, planner, needed)
+        if not outs:
+            return 0
+        kernel = _native.jit_compile(name, src)
+        in_slots = [use(r) for r in ext]
+        out_slots = [define(o) for o in outs]
+        rows = rp.batch
+        grid = max(1, min((rows + 127) // 128, _sm_count(self.dev) * 16))
+        ptrs = in_slots + out_slots
+        n_rng = max(1, len(rng_counts))
+        scalars = struct.pack("<qQ", rows, 0) + b"\0" * (8 * n_rng)
+        payload = struct.pack("<QIIII", kernel, grid, 128, 0, len(ptrs))
+        payload += struct.pack("<%di" % len(ptrs), *ptrs)
+        payload += struct.pack("<I", len(scalars)) + scalars
+        patches = [(0, 8, 0)] + [(1, 16 + 8 * i, c) for i, c in enumerate(rng_counts)]
+        payload += struct.pack("<I", len(patches))
+        for kind, off, count in patches:
+            payload += struct.pack("<IIQ", kind, off, count)
         pw.step(1, payload, defs=out_slots, uses=in_slots)
         return 1
 

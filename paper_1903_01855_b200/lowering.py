@@ -276,6 +276,10 @@ def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
     units: List[Any] = []
     cur: Optional[FusedGroup] = None
     for op in ops:
+        if isinstance(op, tuple):  # (RowProgram, planner) from rowfuse.plan_rows
+            cur = None
+            units.append(op)
+            continue
         if op.kind == "ew" and fuse_enabled:
             shape = op.outs[0].shape
             if cur is not None and cur.shape == shape:
@@ -306,6 +310,27 @@ _UNARY_FN = {
 _BINARY_FN = {"add": "sf::add", "sub": "sf::sub", "mul": "sf::mul", "div": "sf::div",
               "maximum": "sf::maximum", "minimum": "sf::minimum"}
 _COMPARE = {"greater": ">", "less": "<", "equal": "==", "greater_equal": ">="}
+
+
+def ew_expr(nm: str, args: List[str], ct: str) -> str:
+    """C expression of one elementwise op (same functions as the eager kernels)."""
+    if nm == "identity":
+        return args[0]
+    if nm in _UNARY_FN:
+        return f"{_UNARY_FN[nm]}({args[0]})"
+    if nm in _BINARY_FN:
+        return f"{_BINARY_FN[nm]}({args[0]}, {args[1]})"
+    if nm in _COMPARE:
+        return f"({args[0]} {_COMPARE[nm]} {args[1]})"
+    if nm == "isfinite":
+        return f"sf::isfinite_({args[0]})"
+    if nm == "logical_not":
+        return f"(!{args[0]})"
+    if nm == "select":
+        return f"({args[0]} ? {args[1]} : {args[2]})"
+    if nm.startswith("cast_"):
+        return f"({ct})({args[0]})"
+    raise KernelError(f"fusion: no code for elementwise op {nm!r}")
 
 
 def c_literal(value, dtype: DType) -> str:
@@ -393,29 +418,10 @@ def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List
     for t, op in enumerate(group.ops):
         o = op.outs[0]
         ct = _CTYPE[o.dtype]
-        args = [ref(x) for x in op.ins]
         # operands of a broadcasting op that have a different (smaller) shape
         # were loaded through broadcast indexing already (ext inputs), and
         # in-group values always have the group shape.
-        nm = op.name
-        if nm == "identity":
-            expr = args[0]
-        elif nm in _UNARY_FN:
-            expr = f"{_UNARY_FN[nm]}({args[0]})"
-        elif nm in _BINARY_FN:
-            expr = f"{_BINARY_FN[nm]}({args[0]}, {args[1]})"
-        elif nm in _COMPARE:
-            expr = f"({args[0]} {_COMPARE[nm]} {args[1]})"
-        elif nm == "isfinite":
-            expr = f"sf::isfinite_({args[0]})"
-        elif nm == "logical_not":
-            expr = f"(!{args[0]})"
-        elif nm == "select":
-            expr = f"({args[0]} ? {args[1]} : {args[2]})"
-        elif nm.startswith("cast_"):
-            expr = f"({ct})({args[0]})"
-        else:
-            raise KernelError(f"fusion: no code for elementwise op {nm!r}")
+        expr = ew_expr(op.name, [ref(x) for x in op.ins], ct)
         lines.append(f"    const {ct} v{t} = {expr};")
         names[(id(o), o.shape)] = f"v{t}"
     for k, o in enumerate(outs):

@@ -48,3 +48,11 @@ def test_c2_oracle():
 def test_l2hmc_reference_eager_equals_staged(b):
     np.testing.assert_array_equal(GOLD[f"l2hmc_eager_{b}"], GOLD[f"l2hmc_staged_{b}"])
     assert int(GOLD[f"l2hmc_trace_count_{b}"][0]) == 1
+
+
+@pytest.mark.parametrize("b", [16, 200])
+def test_l2hmc_oracle(b):
+    want = GOLD[f"l2hmc_staged_{b}"]
+    m = workloads_np.L2HMC(b, seed=0, runtime_seed=0)
+    got = np.stack([m.transition() for _ in range(3)])
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-6)
