@@ -1,0 +1,411 @@
+"""Benchmark driver (one JSON line on rank 0).
+
+Headline (BASELINE.json metric "L2HMC samples/s ... staged vs eager"):
+the L2HMC sampler (workloads/l2hmc.py) on the 2-D strongly-correlated
+Gaussian, 10 leapfrog steps, staged, 100,000 chains per GPU (config C3's
+largest chain count; weak scaling: N GPUs sample N x 1e5 independent chains,
+no collective).  A step = one full transition (forward + backward
+trajectories, direction draw, MH accept) of every chain.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--chains B]
+    python bench.py --impl reference ...     # the CPU reference arm
+
+``value``: samples/s with the chain state resident in HBM, timed per step
+with CUDA events on the backend's stream (L2 flushed between steps), max
+over ranks.  ``e2e``: the same metric through the public API with the chain
+state uploaded from host memory and the new state + accept probabilities
+read back every step.  Extra keys report config C1 (200 chains) staged and
+eager, the reference-pinned leapfrog workload, and the C2 microbenchmark.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived nominal FP32 SIMT peak
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--chains", type=int, default=100000)
+    ap.add_argument("--quick", action="store_true", help="skip the extra workloads")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work of a traced graph (SURVEY.md §8(d) definition)
+# ---------------------------------------------------------------------------
+
+
+def graph_work(gf):
+    import numpy as np
+
+    flops = 0
+    n_ops = 0
+    for n in gf.nodes:
+        if n.op in ("constant", "reshape", "identity", "transpose", "broadcast_to"):
+            continue
+        n_ops += 1
+        out = n.out_specs[0][1] if n.out_specs else ()
+        if n.op == "matmul":
+            (m, k), (_, nn) = gf.spec_of(n.inputs[0])[1], gf.spec_of(n.inputs[1])[1]
+            flops += 2 * m * k * nn
+        elif n.op in ("reduce_sum", "reduce_mean"):
+            flops += int(np.prod(gf.spec_of(n.inputs[0])[1], dtype=np.int64))
+        else:
+            flops += int(np.prod(out, dtype=np.int64)) if out else 1
+    return flops, n_ops
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port on host cores
+# ---------------------------------------------------------------------------
+
+
+def _port_shard(args):
+    chains, seed, transitions = args
+    import numpy as np
+
+    from oracle import workloads_np
+
+    m = workloads_np.L2HMC(chains, seed=seed, runtime_seed=seed)
+    t = time.perf_counter()
+    for _ in range(transitions):
+        m.transition()
+    return time.perf_counter() - t
+
+
+def cpu_port_rate(chains: int, transitions: int, workers: int):
+    """samples/s of the NumPy oracle port, chains sharded over `workers` processes."""
+    import multiprocessing as mp
+
+    per = max(1, chains // workers)
+    jobs = [(per, 1000 + i, transitions) for i in range(workers)]
+    t = time.perf_counter()
+    if workers == 1:
+        _port_shard(jobs[0])
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:
+            pool.map(_port_shard, jobs)
+    dt = time.perf_counter() - t
+    return per * workers * transitions / dt, dt
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    sample = min(a.chains, 20000)
+    rates = []
+    for i in range(a.warmup + a.steps):
+        r, _ = cpu_port_rate(sample, 1, cores)
+        if i >= a.warmup:
+            rates.append(r)
+    value = sum(rates) / len(rates)
+    line = {
+        "impl": "reference", "metric": "l2hmc_samples_per_sec", "value": value,
+        "unit": "samples/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "l2hmc_sampler_staged", "chains_per_gpu": a.chains,
+                   "leapfrog_steps": 10, "x_dim": 2, "hidden": 10},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} chains x 1 transition per step, numpy oracle port "
+                                   f"(oracle/workloads_np.py L2HMC) sharded over {cores} processes"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(a, rank, world, dist):
+    import numpy as np
+    import torch
+
+    import paper_1903_01855_b200 as sf
+    from paper_1903_01855_b200 import _native, plugins
+    from paper_1903_01855_b200.workloads import l2hmc
+
+    assert _native.device_count() > 0, "no CUDA device"
+    sf.init_runtime(sf.RuntimeOptions(seed=1234 + rank))
+    plugins.install()
+    dev = 0
+    stream = torch.cuda.ExternalStream(_native.stream_of(dev))
+    peaks, peak_kind = _peaks()
+
+    B = a.chains
+    sampler = l2hmc.L2HMCSampler(sf, B, "staged", seed=rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        _native.sync(dev)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    t0 = time.perf_counter()
+    for _ in range(a.warmup):
+        sampler.step()
+    _native.sync(dev)
+    warm_s = time.perf_counter() - t0
+    cf = sampler.transition.cached_functions()[0]
+    prog = next(iter(cf.graph._plan.values()))
+    flops_per_step, n_graph_ops = graph_work(cf.graph)
+
+    # -- value: device-resident state, per-step CUDA events, L2 flushed between steps
+    barrier()
+    launches0 = _native.launch_count(dev)
+    times = []
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for _ in range(a.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)  # > L2 (126 MB)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            sampler.step()
+            e1.record(stream)
+            times.append((e0, e1))
+        _native.sync(dev)
+        torch.cuda.synchronize()
+    launches = _native.launch_count(dev) - launches0 - 0
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in times]
+    total_s = sum(step_ms) / 1e3
+    if dist is not None:
+        t = torch.tensor([total_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    barrier()
+    value = B * world * a.steps / total_s
+    ms_per_step = total_s * 1e3 / a.steps
+
+    # -- roofline of the dominant kernel: per-launch GPU time from plan events
+    seg = prog.segments[0]
+    seg.plan.profile(True)
+    for _ in range(3):
+        sampler.step()
+    stats = seg.plan.step_stats()
+    seg.plan.profile(False)
+    jit_ms = [ms / runs for kind, ms, runs in stats if kind == 1 and runs]
+    kern_ms = sum(jit_ms)
+    achieved = flops_per_step / (kern_ms / 1e3) / 1e12 if kern_ms else 0.0
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": FFMA_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FFMA_PEAK_TFLOPS, "traffic": None,
+                "peak_kind": "derived nominal FP32 SIMT (148 SM x 128 lanes x 2 x 1.965 GHz); "
+                             "the row program has no tensor-core-shaped work (K<=10 per chain)",
+                "kernels_per_step": len(jit_ms), "kernel_ms_per_step": kern_ms,
+                "algorithmic_flops_per_step": flops_per_step,
+                "flops_per_chain": flops_per_step / B,
+                "hbm_bytes_per_step": B * (8 + 8 + 4),
+                "hbm_frac": B * 20 / (kern_ms / 1e3) / (peaks["hbm_gbs"] * 1e9) if kern_ms else 0}
+
+    # -- e2e through the public API: state from pinned host memory, results read back
+    x_host = torch.from_numpy(sampler.x.numpy()).pin_memory()
+    e2e_ms = []
+    barrier()
+    for _ in range(a.steps):
+        t = time.perf_counter()
+        x = sf.tensor_from_host(x_host.numpy(), (B, 2), sf.float32)
+        x_out, acc = sampler.transition(x)
+        xo, ao = x_out.numpy(), acc.numpy()
+        e2e_ms.append((time.perf_counter() - t) * 1e3)
+        x_host.copy_(torch.from_numpy(xo))
+    e2e_s = sum(e2e_ms) / 1e3
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": B * world * a.steps / e2e_s, "unit": "samples/s",
+           "h2d_bytes_per_step": B * 2 * 4, "d2h_bytes_per_step": B * 2 * 4 + B * 4}
+
+    extra = {}
+    if rank == 0 and world == 1 and not a.quick:
+        extra = extras(sf, np, _native, plugins, l2hmc)
+    cpu = None
+    if rank == 0 and world == 1:
+        cores = os.cpu_count() or 1
+        sample = 20000
+        r, dt = cpu_port_rate(sample, 1, cores)
+        cpu = {"value": r, "unit": "samples/s", "cores": cores, "kind": "port",
+               "sample": f"{sample} chains x 1 transition ({dt:.1f}s), numpy oracle port sharded "
+                         f"over {cores} processes"}
+    if rank != 0:
+        return
+    line = {
+        "metric": "l2hmc_samples_per_sec", "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (random-init L2HMC nets, N(0,1) initial chains)",
+        "config": {"workload": "l2hmc_sampler_staged", "chains_per_gpu": B,
+                   "global_chains": B * world, "leapfrog_steps": 10, "x_dim": 2, "hidden": 10,
+                   "parallelism": f"dp{world} (independent chains, no collective)",
+                   "l2_flush": "256 MiB fill between timed steps",
+                   "rng": "device Philox"},
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+        "gpu_launches": launches, "gpu_launches_per_step": launches / a.steps,
+        "clocks": clk.summary(), "trace_and_compile_s": warm_s,
+        "graph_ops": n_graph_ops, "native_launches_per_step": prog.n_launches,
+        "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "kind": peak_kind},
+        "extra": extra,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _time_steps(fn, n, _native, warm=2):
+    for _ in range(warm):
+        fn()
+    _native.sync(0)
+    t = time.perf_counter()
+    for _ in range(n):
+        fn()
+    _native.sync(0)
+    return (time.perf_counter() - t) / n
+
+
+def extras(sf, np, _native, plugins, l2hmc):
+    """Secondary configs (wall-clock per step incl. Python dispatch)."""
+    from paper_1903_01855_b200.workloads.leapfrog import Leapfrog
+    from paper_1903_01855_b200.workloads import microbench
+
+    out = {}
+    # C1: L2HMC 200 chains, staged vs eager
+    c1 = {}
+    for mode, n in (("staged", 50), ("eager", 3)):
+        sf.init_runtime(sf.RuntimeOptions(seed=7))
+        plugins.install()
+        s = l2hmc.L2HMCSampler(sf, 200, mode, seed=0)
+        dt = _time_steps(s.step, n, _native)
+        c1[mode] = {"samples_per_sec": 200 / dt, "ms_per_transition": dt * 1e3}
+    c1["staged_over_eager"] = c1["staged"]["samples_per_sec"] / c1["eager"]["samples_per_sec"]
+    out["c1_l2hmc_200_chains"] = c1
+    # reference-pinned leapfrog (stageflow/bench.py:147-183)
+    lf = {}
+    for b in (200, 100000, 10000000):
+        row = {}
+        for mode in ("staged", "eager"):
+            if mode == "eager" and b > 100000:
+                continue
+            sf.init_runtime(sf.RuntimeOptions())
+            wl = Leapfrog(b, mode)
+            dt = _time_steps(wl.step, 50 if mode == "staged" else 3, _native)
+            row[mode] = {"chains_per_sec": b / dt, "us_per_trajectory": dt * 1e6}
+        if "eager" in row:
+            row["staged_over_eager"] = row["staged"]["chains_per_sec"] / row["eager"]["chains_per_sec"]
+        row["staged"]["hbm_gbs_wall"] = 32 * b / (row["staged"]["us_per_trajectory"] * 1e-6) / 1e9
+        lf[str(b)] = row
+    out["leapfrog"] = lf
+    # C2 microbenchmark: 100 x (matmul + add + tanh), primitive ops/s
+    c2 = {}
+    for mode, n in (("staged", 50), ("eager", 3)):
+        sf.init_runtime(sf.RuntimeOptions())
+        plugins.install()
+        mb = microbench.Chain(mode)
+        dt = _time_steps(mb.step, n, _native)
+        c2[mode] = {"ops_per_sec": 300 / dt, "us_per_op": dt * 1e6 / 300}
+    c2["staged_over_eager"] = c2["staged"]["ops_per_sec"] / c2["eager"]["ops_per_sec"]
+    out["c2_microbench"] = c2
+    return out
+
+
+def main():
+    a = _args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        os.environ["CUDA_VISIBLE_DEVICES"] = str(local)
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(0)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    run_ours(a, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -133,6 +133,11 @@ int sf_plan_create(int dev, const void* desc, size_t desc_bytes, void** plan);
  * passes to the caller, release with sf_free). */
 int sf_plan_run(void* plan, const void* const* inputs, void** outputs);
 int sf_plan_info(void* plan, int* n_inputs, int* n_outputs, int* n_steps, int* n_launches);
+/* Per-step GPU timing: when enabled, every run brackets each step with CUDA
+ * events on the device stream, synchronises, and accumulates the durations
+ * (measurement aid for the roofline; adds a stream sync per run). */
+int sf_plan_profile(void* plan, int enable);
+int sf_plan_step_stats(void* plan, int step, int* kind, double* total_ms, uint64_t* runs);
 int sf_plan_destroy(void* plan);
 
 /* ------------------------------------------------------- counters */

@@ -89,6 +89,10 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_plan_run": (ctypes.c_int, [_VP, _VP, _VP]),
         "sf_plan_info": (ctypes.c_int, [_VP] + [ctypes.POINTER(ctypes.c_int)] * 4),
         "sf_plan_destroy": (ctypes.c_int, [_VP]),
+        "sf_plan_profile": (ctypes.c_int, [_VP, ctypes.c_int]),
+        "sf_plan_step_stats": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                               ctypes.POINTER(ctypes.c_double),
+                                               ctypes.POINTER(ctypes.c_uint64)]),
         "sf_launch_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
     }
     for name, (res, args) in sig.items():
@@ -104,6 +108,7 @@ EXPORTED_SYMBOLS = (
     "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
+    "sf_plan_profile", "sf_plan_step_stats",
 )
 
 
@@ -435,6 +440,23 @@ class NativePlan:
             if rc:
                 raise _err(_lib, rc, "plan run")
             return outs[: self.n_out]
+
+    def profile(self, enable: bool) -> None:
+        rc = _lib.sf_plan_profile(self.handle, int(enable))
+        if rc:
+            raise _err(_lib, rc, "plan profile")
+
+    def step_stats(self) -> List[tuple]:
+        """[(step kind, total ms, runs)] accumulated while profiling."""
+        n = ctypes.c_int(0)
+        _lib.sf_plan_info(self.handle, None, None, ctypes.byref(n), None)
+        out = []
+        kind, ms, runs = ctypes.c_int(0), ctypes.c_double(0), ctypes.c_uint64(0)
+        for s in range(n.value):
+            _lib.sf_plan_step_stats(self.handle, s, ctypes.byref(kind), ctypes.byref(ms),
+                                    ctypes.byref(runs))
+            out.append((kind.value, ms.value, runs.value))
+        return out
 
     def __del__(self):
         h = self.handle

@@ -66,6 +66,12 @@ struct Step {
 
 struct Plan {
   int dev = 0;
+  // optional per-step GPU timing (sf_plan_profile): CUDA events around each
+  // step, read back after the run's stream synchronisation
+  bool profile = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<double> step_ms;
+  std::vector<uint64_t> step_runs;
   std::vector<Slot> slots;
   std::vector<Step> steps;
   std::vector<int32_t> input_slot;   // input ordinal -> slot
@@ -306,8 +312,10 @@ int sf_plan_run(void* plan, const void* const* inputs, void** outputs) {
       if (st != SF_OK) break;
     }
     if (st != SF_OK) break;
+    if (p->profile) cudaEventRecord(p->ev[2 * k], d->stream);
     st = run_step(p, d, s, ptr);
     if (st != SF_OK) break;
+    if (p->profile) cudaEventRecord(p->ev[2 * k + 1], d->stream);
     for (int32_t slot : s.frees) {
       d->alloc.release(ptr[slot]);
       ptr[slot] = nullptr;
@@ -324,6 +332,39 @@ int sf_plan_run(void* plan, const void* const* inputs, void** outputs) {
     return st;
   }
   for (size_t o = 0; o < p->output_slot.size(); ++o) outputs[o] = ptr[p->output_slot[o]];
+  if (p->profile) {
+    SF_CHECK_CUDA(cudaStreamSynchronize(d->stream));
+    for (size_t j = 0; j < p->steps.size(); ++j) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p->ev[2 * j], p->ev[2 * j + 1]) == cudaSuccess) {
+        p->step_ms[j] += ms;
+        p->step_runs[j] += 1;
+      }
+    }
+  }
+  return SF_OK;
+}
+
+int sf_plan_profile(void* plan, int enable) {
+  Plan* p = (Plan*)plan;
+  Device* d;
+  SF_TRY(ensure_device(p->dev, &d));
+  if (enable && p->ev.empty()) {
+    p->ev.resize(2 * p->steps.size());
+    for (auto& e : p->ev) SF_CHECK_CUDA(cudaEventCreate(&e));
+  }
+  p->step_ms.assign(p->steps.size(), 0.0);
+  p->step_runs.assign(p->steps.size(), 0);
+  p->profile = enable != 0;
+  return SF_OK;
+}
+
+int sf_plan_step_stats(void* plan, int step, int* kind, double* total_ms, uint64_t* runs) {
+  Plan* p = (Plan*)plan;
+  if (step < 0 || step >= (int)p->steps.size()) return SF_ERR_INVALID;
+  if (kind) *kind = (int)p->steps[step].kind;
+  if (total_ms) *total_ms = p->step_ms.empty() ? 0.0 : p->step_ms[step];
+  if (runs) *runs = p->step_runs.empty() ? 0 : p->step_runs[step];
   return SF_OK;
 }
 

@@ -137,6 +137,7 @@ class Program:
             for op in _unit_ops(unit):
                 for o in op.outs:
                     produced_in[id(o)] = u
+        self._precompile_rows(units, last_use)
 
         segs: list = []
         run: list = []
@@ -160,6 +161,25 @@ class Program:
                 run.append(unit)
         flush(len(units))
         return segs
+
+    @staticmethod
+    def _precompile_rows(units, last_use) -> None:
+        """Generate every row-program chunk and compile them on parallel threads."""
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+
+        from .rowfuse import generate_rowprog
+
+        jobs = []
+        for u, unit in enumerate(units):
+            if isinstance(unit, tuple):
+                needed = {id(o) for op in unit[0].ops for o in op.outs
+                          if last_use.get(id(o), -1) > u}
+                name, src = generate_rowprog(unit[0], unit[1], needed)[:2]
+                jobs.append((name, src))
+        if len(jobs) > 1:
+            with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
+                list(pool.map(lambda j: _native.jit_compile(*j), jobs))
 
     def _build_native(self, units, start, stop, last_use, produced_in) -> _NativeSegment:
         pw = PlanWriter()
@@ -252,11 +272,12 @@ class Program:
         in_slots = [use(r) for r in ext]
         out_slots = [define(o) for o in outs]
         rows = rp.batch
-        grid = max(1, min((rows + 127) // 128, _sm_count(self.dev) * 16))
+        grid = 1 if rp.uniform_only else max(1, (rows + 127) // 128)  # one chain per thread
         ptrs = in_slots + out_slots
         n_rng = max(1, len(rng_counts))
         scalars = struct.pack("<qQ", rows, 0) + b"\0" * (8 * n_rng)
-        payload = struct.pack("<QIIII", kernel, grid, 128, 0, len(ptrs))
+        block = 32 if rp.uniform_only else 128  # uniform kernels are one warp
+        payload = struct.pack("<QIIII", kernel, grid, block, 0, len(ptrs))
         payload += struct.pack("<%di" % len(ptrs), *ptrs)
         payload += struct.pack("<I", len(scalars)) + scalars
         patches = [(0, 8, 0)] + [(1, 16 + 8 * i, c) for i, c in enumerate(rng_counts)]

@@ -34,12 +34,46 @@ MAX_SMEM_BYTES = 40 * 1024     # uniform inputs staged in shared memory
 MIN_BATCH = 2
 
 
+# NVVM compile time grows superlinearly with function size, so a long row
+# program is cut into chunks of about this many scalar operations; each
+# chunk is its own kernel (rowed values crossing a cut round-trip through
+# L2-resident temporaries) and the chunks compile in parallel.
+CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "1200"))
+# CTAs of 128 threads that must fit per SM (register budget = 64K / (128 * MIN_BLOCKS))
+MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "2"))
+
+
 class RowProgram:
-    __slots__ = ("ops", "batch")
+    __slots__ = ("ops", "batch", "gen", "uniform_only")
 
     def __init__(self, batch: int):
         self.ops: List[LOp] = []
         self.batch = batch
+        self.gen = None  # cached generate_rowprog result
+        self.uniform_only = False  # single-CTA kernel for chain-independent ops
+
+
+def _op_cost(op: LOp, planner) -> int:
+    o = op.outs[0]
+    L = planner.layout_of(o)
+    width = L[1] if L[0] == ROW else max(1, o.numel)
+    if op.kind == "matmul":
+        return op.ins[0].shape[-1] * width
+    return width
+
+
+def _split(rp: RowProgram, planner) -> List[RowProgram]:
+    chunks, cur, cost = [], RowProgram(rp.batch), 0
+    for op in rp.ops:
+        c = _op_cost(op, planner)
+        if cur.ops and cost + c > CHUNK_COST:
+            chunks.append(cur)
+            cur, cost = RowProgram(rp.batch), 0
+        cur.ops.append(op)
+        cost += c
+    if cur.ops:
+        chunks.append(cur)
+    return chunks
 
 
 ROW, UNI, BAD = "row", "uni", "bad"
@@ -150,9 +184,9 @@ def choose_batch(ops: List[LOp]) -> int:
 def plan_rows(ops: List[LOp]) -> List:
     """Split ops into RowPrograms (runs of row-local ops) and plain ops."""
     batch = choose_batch(ops)
-    if batch < MIN_BATCH:
-        return list(ops)
-    planner = RowPlanner(batch)
+    # no batch dimension (e.g. the C2 chain on (1, 16)): every value is uniform
+    # and runs of small ops become one-warp uniform kernels
+    planner = RowPlanner(batch if batch >= MIN_BATCH else -1)
     units: List = []
     cur: Optional[RowProgram] = None
     for op in ops:
@@ -171,14 +205,35 @@ def plan_rows(ops: List[LOp]) -> List:
     out: List = []
     for u in units:
         if isinstance(u, RowProgram):
-            n_row = sum(1 for op in u.ops if planner.layout_of(op.outs[0])[0] == ROW)
-            if n_row >= 2 and _smem_bytes(u, planner) <= MAX_SMEM_BYTES:
+            row_ops = [op for op in u.ops if planner.layout_of(op.outs[0])[0] == ROW]
+            if len(row_ops) >= 2:
+                # chain-independent (uniform) ops never depend on rowed values, so
+                # they are hoisted into one single-CTA kernel run once per call
+                uni = RowProgram(u.batch)
+                uni.ops = [op for op in u.ops if planner.layout_of(op.outs[0])[0] != ROW]
+                uni.uniform_only = True
+                body = RowProgram(u.batch)
+                body.ops = row_ops
+                chunks = _split(body, planner)
+                if (all(_smem_bytes(c, planner) <= MAX_SMEM_BYTES for c in chunks)
+                        and _uniform_smem(uni) <= MAX_SMEM_BYTES):
+                    if uni.ops:
+                        out.append((uni, planner))
+                    out.extend((c, planner) for c in chunks)
+                    continue
+            elif not row_ops and len(u.ops) >= 2 and _uniform_smem(u) <= MAX_SMEM_BYTES:
+                u.uniform_only = True
                 out.append((u, planner))
                 continue
             out.extend(u.ops)
         else:
             out.append(u)
     return out
+
+
+def _uniform_smem(rp: RowProgram) -> int:
+    """Shared memory a uniform kernel needs for its computed values."""
+    return sum(o.nbytes for op in rp.ops for o in op.outs)
 
 
 def _smem_bytes(rp: RowProgram, planner: RowPlanner) -> int:
@@ -210,6 +265,7 @@ class _Gen:
         self.ext_kind: List[str] = []    # "row" | "uni"
         self.ptr_of: Dict[int, int] = {}
         self.prologue: List[str] = []
+        self.dirty: set = set()   # uniform values written since the last __syncthreads
         self.smem: List[str] = []
         self.body: List[str] = []
         self.rowed_names: Dict[int, List[str]] = {}
@@ -239,10 +295,13 @@ class _Gen:
             self.body.append("    " + " ".join(
                 f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{idx} + {j}];" if w > 1 else
                 f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[r];" for j, nm in enumerate(names)))
+        elif self.rp.uniform_only:
+            # uniform kernel: loops read straight from global memory (uni_ref)
+            self.ext_kind.append(UNI)
         else:
             self.ext_kind.append(UNI)
             n = r.numel
-            self.smem.append(f"  __shared__ {ct} s{k}[{max(1, n)}];\n"
+            self.smem.append(f"  __shared__ __align__(16) {ct} s{k}[{max(1, n)}];\n"
                              f"  for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
                              f"s{k}[q] = ((const {ct}*)a.p[{k}])[q];")
             self.uni_names[id(r)] = [f"s{k}[{q}]" for q in range(n)]
@@ -253,6 +312,89 @@ class _Gen:
             return c_literal(r.imm, r.dtype)
         names = self.uni_names[id(r)]
         return names[flat]
+
+    def uni_ref(self, x: LV, idx: str) -> str:
+        """Uniform element at a run-time flat index (uniform-kernel loops)."""
+        r = x.root()
+        if r.kind == "const" and r.imm is not None:
+            return c_literal(r.imm, r.dtype)
+        if id(r) in self.ptr_of and id(r) not in self.produced:
+            k = self.ptr_of[id(r)]
+            ct = _CTYPE[r.dtype]
+            if ct == "bool":
+                return f"((const bool*)a.p[{k}])[{idx}]"
+            return f"__ldg((const {ct}*)a.p[{k}] + ({idx}))"
+        return f"U{r.id}[{idx}]"
+
+    def _emit_uniform_loop(self, op: LOp) -> None:
+        """Uniform op in the one-warp uniform kernel: a generated loop over the
+        output elements (lanes take consecutive elements, no divergence), the
+        result in shared memory; __syncwarp only before reading fresh values."""
+        from .lowering import _index_expr
+
+        o = op.outs[0]
+        ct = _CTYPE[o.dtype]
+        n = o.numel
+        if any(id(x.root()) in self.dirty for x in op.ins):
+            self.prologue.append("  __syncwarp();")
+            self.dirty.clear()
+        self.smem.append(f"  __shared__ __align__(16) {ct} U{o.id}[{max(1, n)}];")
+        self.uni_names[id(o)] = [f"U{o.id}[{q}]" for q in range(n)]
+        self.dirty.add(id(o))
+        k = op.kind
+        shape = o.shape
+        loop = f"  for (int f = threadIdx.x; f < {n}; f += 32) {{ "
+        if k == "ew":
+            args = [self.uni_ref(x, _index_expr(x.shape, shape, "f") if x.numel != 1 else "0")
+                    for x in op.ins]
+            body = f"U{o.id}[f] = {ew_expr(op.name, args, ct)};"
+        elif k == "matmul":
+            a, b = op.ins
+            m, kk_n = a.shape
+            nn = b.shape[1]
+            fma = "__fmaf_rn" if o.dtype is DType.float32 else "__fma_rn"
+            body = (f"const int i = f / {nn}, j = f % {nn}; {ct} acc = ({ct})0; "
+                    f"for (int k = 0; k < {kk_n}; ++k) acc = {fma}("
+                    f"{self.uni_ref(a, f'i * {kk_n} + k')}, {self.uni_ref(b, f'k * {nn} + j')}, acc); "
+                    f"U{o.id}[f] = acc;")
+        elif k == "transpose":
+            x = op.ins[0]
+            rows, cols = x.shape
+            body = (f"const int j = f / {rows}, i = f % {rows}; "
+                    f"U{o.id}[f] = {self.uni_ref(x, f'i * {cols} + j')};")
+        elif k == "eye":
+            m = shape[0]
+            body = f"U{o.id}[f] = ({ct})(f / {m} == f % {m} ? 1 : 0);"
+        elif k == "reduce":
+            x = op.ins[0]
+            axes = tuple(op.attrs["axes"])
+            xs = x.shape
+            kept = [d for d in range(len(xs)) if d not in axes]
+            red = [d for d in range(len(xs)) if d in axes]
+            xst = _strides_for(xs, xs)
+            count = dtypes.element_count([xs[d] for d in red])
+            # offset of reduced element g (row-major over reduced dims) for output f
+            terms, inner = [], 1
+            for d in reversed(kept):
+                terms.append(f"((f / {inner}) % {xs[d]}) * {xst[d]}")
+                inner *= xs[d]
+            inner = 1
+            for d in reversed(red):
+                terms.append(f"((g / {inner}) % {xs[d]}) * {xst[d]}")
+                inner *= xs[d]
+            off = " + ".join(terms) if terms else "0"
+            p = min(count, 32)
+            scale = f" / ({ct}){float(count)!r}" if op.name == "reduce_mean" else ""
+            body = (f"{ct} acc[32]; "
+                    f"for (int l = 0; l < {p}; ++l) {{ int g = l; acc[l] = {self.uni_ref(x, off)}; "
+                    f"for (g = l + 32; g < {count}; g += 32) acc[l] = sf::add(acc[l], "
+                    f"{self.uni_ref(x, off)}); }} "
+                    f"for (int s = 16; s >= 1; s >>= 1) for (int l = 0; l < s; ++l) "
+                    f"if (l + s < {p}) acc[l] = sf::add(acc[l], acc[l + s]); "
+                    f"U{o.id}[f] = acc[0]{scale};")
+        else:
+            raise KernelError(f"uniform kernel: unsupported op {k}")
+        self.prologue.append(loop + body + " }")
 
     def row_elem(self, x: LV, j: int, out_w: int, out_rank: int) -> str:
         """Element of operand x for output column j of a rowed op."""
@@ -275,7 +417,9 @@ class _Gen:
                 self._input(x)
             L = self.P.layout_of(op.outs[0])
             if L[0] == UNI:
-                self._emit_uniform(op)
+                if not self.rp.uniform_only:
+                    raise KernelError("row program: uniform ops belong in the uniform kernel")
+                self._emit_uniform_loop(op)
             else:
                 self._emit_rowed(op, L)
         for op in self.rp.ops:
@@ -330,6 +474,10 @@ class _Gen:
             n = b.shape[1]
             fma = "__fmaf_rn" if o.dtype is DType.float32 else "__fma_rn"
             xs = [self.row_elem(a, kk, kk_n, 2) for kk in range(kk_n)]
+            # compiler-only memory fence: keeps NVVM from merging this matvec's
+            # weight loads with other uses of the same weights (which would pin
+            # hundreds of weights in registers for the whole chunk)
+            lines.append('asm volatile("" ::: "memory");')
             for j in range(n):
                 acc = f"({ct})0"
                 for kk in range(kk_n):
@@ -357,77 +505,12 @@ class _Gen:
                 lines.append(f"const {ct} {names[j]} = {val};")
         else:
             raise KernelError(f"row program: unsupported rowed op {k}")
+        if id(o) in self.needed:
+            # store right at the definition so the value's registers free up
+            for j, nm in enumerate(names):
+                idx = "r" if w == 1 else f"r * {w} + {j}"
+                lines.append(f"(({ct}*)a.p[@O{o.id}@])[{idx}] = {nm};")
         self.body.append("    " + "\n    ".join(lines))
-
-    def _emit_uniform(self, op: LOp) -> None:
-        o = op.outs[0]
-        ct = _CTYPE[o.dtype]
-        n = o.numel
-        names = [f"u{o.id}_{q}" for q in range(n)]
-        self.uni_names[id(o)] = names
-        lines = []
-        k = op.kind
-        shape = o.shape
-        if k == "ew":
-            strides = [(_strides_for(x.shape, shape) if x.numel != 1 else None) for x in op.ins]
-            for f in range(n):
-                idx = _unflatten(f, shape)
-                args = []
-                for x, st in zip(op.ins, strides):
-                    src = 0 if st is None else sum(i * s for i, s in zip(idx, st))
-                    args.append(self.uni_elem(x, src))
-                lines.append(f"const {ct} {names[f]} = {ew_expr(op.name, args, ct)};")
-        elif k == "matmul":
-            a, b = op.ins
-            m, kk_n = a.shape
-            nn = b.shape[1]
-            fma = "__fmaf_rn" if o.dtype is DType.float32 else "__fma_rn"
-            for i in range(m):
-                for j in range(nn):
-                    acc = f"({ct})0"
-                    for kk in range(kk_n):
-                        acc = f"{fma}({self.uni_elem(a, i * kk_n + kk)}, {self.uni_elem(b, kk * nn + j)}, {acc})"
-                    lines.append(f"const {ct} {names[i * nn + j]} = {acc};")
-        elif k == "transpose":
-            x = op.ins[0]
-            rows, cols = x.shape
-            for i in range(rows):
-                for j in range(cols):
-                    lines.append(f"const {ct} {names[j * rows + i]} = {self.uni_elem(x, i * cols + j)};")
-        elif k == "eye":
-            m = shape[0]
-            for f in range(n):
-                lines.append(f"const {ct} {names[f]} = ({ct}){1 if f // m == f % m else 0};")
-        elif k == "reduce":
-            x = op.ins[0]
-            axes = tuple(op.attrs["axes"])
-            xs = x.shape
-            kept = [d for d in range(len(xs)) if d not in axes]
-            red = [d for d in range(len(xs)) if d in axes]
-            xst = _strides_for(xs, xs)
-            for f in range(n):
-                # output flat f -> kept coordinates
-                kshape = [xs[d] for d in kept]
-                kidx = _unflatten(f, kshape) if kshape else []
-                rshape = [xs[d] for d in red]
-                count = dtypes.element_count(rshape)
-                elems = []
-                for g in range(count):
-                    ridx = _unflatten(g, rshape) if rshape else []
-                    full = [0] * len(xs)
-                    for d, v in zip(kept, kidx):
-                        full[d] = v
-                    for d, v in zip(red, ridx):
-                        full[d] = v
-                    elems.append(self.uni_elem(x, sum(i * s for i, s in zip(full, xst))))
-                total = self._cro(elems, ct, lines)
-                if op.name == "reduce_mean":
-                    lines.append(f"const {ct} {names[f]} = {total} / ({ct}){float(count)!r};")
-                else:
-                    lines.append(f"const {ct} {names[f]} = {total};")
-        else:
-            raise KernelError(f"row program: unsupported uniform op {k}")
-        self.prologue.append("  " + "\n  ".join(lines))
 
 
 def _unflatten(f: int, shape) -> List[int]:
@@ -439,7 +522,13 @@ def _unflatten(f: int, shape) -> List[int]:
 
 
 def generate_rowprog(rp: RowProgram, planner: RowPlanner, needed: set):
-    """Returns (name, source, in_roots, out_lvs, rng_counts)."""
+    """Returns (name, source, in_roots, out_lvs, rng_counts, n_ptr); cached on rp."""
+    if rp.gen is None:
+        rp.gen = _generate(rp, planner, needed)
+    return rp.gen
+
+
+def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
     g = _Gen(rp, planner, needed)
     g.emit()
     stores = []
@@ -449,28 +538,41 @@ def generate_rowprog(rp: RowProgram, planner: RowPlanner, needed: set):
         ct = _CTYPE[o.dtype]
         L = planner.layout_of(o)
         if L[0] == ROW:
-            w = L[1]
-            for j, nm in enumerate(g.rowed_names[id(o)]):
-                idx = "r" if w == 1 else f"r * {w} + {j}"
-                stores.append(f"(({ct}*)a.p[{k0 + t}])[{idx}] = {nm};")
+            token = f"@O{o.id}@"
+            g.body = [b.replace(token, str(k0 + t)) for b in g.body]
         else:
-            for q, nm in enumerate(g.uni_names[id(o)]):
-                uni_stores.append(f"(({ct}*)a.p[{k0 + t}])[{q}] = {nm};")
+            n = o.numel
+            src_arr = g.uni_names[id(o)][0].split("[")[0]
+            uni_stores.append(f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
+                              f"(({ct}*)a.p[{k0 + t}])[q] = {src_arr}[q];")
     n_ptr = k0 + len(g.outs)
     n_rng = max(1, len(g.rng_ops))
     src = [f"struct Params {{ void* p[{max(1, n_ptr)}]; long long rows; "
            f"unsigned long long seed; unsigned long long off[{n_rng}]; }};",
-           "extern \"C\" __global__ void __launch_bounds__(128) KNAME(const __grid_constant__ Params a) {"]
-    src += g.smem
-    if g.smem:
+           f"extern \"C\" __global__ void __launch_bounds__("
+           f"{'128' if MIN_BLOCKS == 0 else f'128, {MIN_BLOCKS}'}) KNAME(const "
+           "__grid_constant__ Params a) {"]
+    decls = [x for x in g.smem if "for (int q" not in x]
+    loads = [x for x in g.smem if "for (int q" in x]
+    src += decls + loads
+    if loads:
         src.append("  __syncthreads();")
     src += g.prologue
+    if g.prologue:
+        src.append("  __syncthreads();")
     if uni_stores:
-        src.append("  if (blockIdx.x == 0 && threadIdx.x == 0) {\n    " +
-                   "\n    ".join(uni_stores) + "\n  }")
-    src.append("  const long long stride = (long long)gridDim.x * blockDim.x;")
-    src.append("  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; "
-               "r < a.rows; r += stride) {")
+        src.append("  if (blockIdx.x == 0) {\n    " + "\n    ".join(uni_stores) + "\n  }")
+    if rp.uniform_only:
+        src.append("}\n")
+        core = "\n".join(src)
+        name = "sf_uni_" + hashlib.sha1(core.encode()).hexdigest()[:16]
+        source = '#include "sf_ops.cuh"\n' + core.replace("KNAME", name)
+        return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr
+    # one chain per thread, no loop: nothing is loop-invariant, so nothing
+    # gets hoisted into (and pinned in) registers for the whole kernel
+    src.append("  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;")
+    src.append("  if (r >= a.rows) return;")
+    src.append("  {")
     src += g.body
     if stores:
         src.append("    " + "\n    ".join(stores))

@@ -83,7 +83,10 @@ def test_l2hmc_staged_row_program():
     s = l2hmc.L2HMCSampler(sf, 512, "staged", seed=0)
     s.step()
     prog = next(iter(s.transition.cached_functions()[0].graph._plan.values()))
-    assert prog.n_launches <= 4, prog.n_launches
+    n_nodes = len(s.transition.cached_functions()[0].graph.nodes)
+    # ~3300 graph nodes -> one uniform kernel + a few dozen row-program chunks
+    assert prog.n_launches <= 64 < n_nodes, (prog.n_launches, n_nodes)
+    assert len(prog.segments) == 1
 
 
 def test_l2hmc_oracle_host_rng_long_run():
