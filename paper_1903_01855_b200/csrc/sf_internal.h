@@ -93,6 +93,15 @@ struct Device {
   char* pinned = nullptr;
   cudaEvent_t slot_ready[kStageSlots] = {};
   int next_slot = 0;
+  // pinned bounce buffer for large host->device writes (grown on demand),
+  // guarded by the event of the last transfer that read it
+  char* pinned_h2d = nullptr;
+  size_t pinned_h2d_bytes = 0;
+  cudaEvent_t h2d_ready = nullptr;
+  // pinned bounce buffer for large device->host reads (grown on demand)
+  std::mutex d2h_mu;
+  char* pinned_d2h = nullptr;
+  size_t pinned_d2h_bytes = 0;
   int sm_count = 0;
   // device RNG (Philox) state: seed and next counter offset
   unsigned long long rng_seed = 0;

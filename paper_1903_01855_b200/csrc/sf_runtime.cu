@@ -290,6 +290,23 @@ int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes) {
     SF_CHECK_CUDA(cudaEventRecord(d->slot_ready[k], d->stream));
     return SF_OK;
   }
+  if (bytes <= (256u << 20)) {
+    // larger transfers: one pinned bounce buffer, asynchronous w.r.t. the stream
+    std::lock_guard<std::mutex> lk(d->stage_mu);
+    if (d->h2d_ready) SF_CHECK_CUDA(cudaEventSynchronize(d->h2d_ready));
+    else SF_CHECK_CUDA(cudaEventCreateWithFlags(&d->h2d_ready, cudaEventDisableTiming));
+    if (d->pinned_h2d_bytes < bytes) {
+      if (d->pinned_h2d) cudaFreeHost(d->pinned_h2d);
+      size_t want = 1u << 20;
+      while (want < bytes) want <<= 1;
+      SF_CHECK_CUDA(cudaMallocHost((void**)&d->pinned_h2d, want));
+      d->pinned_h2d_bytes = want;
+    }
+    std::memcpy(d->pinned_h2d, src, bytes);
+    SF_CHECK_CUDA(cudaMemcpyAsync(dst, d->pinned_h2d, bytes, cudaMemcpyHostToDevice, d->stream));
+    SF_CHECK_CUDA(cudaEventRecord(d->h2d_ready, d->stream));
+    return SF_OK;
+  }
   SF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, d->stream));
   SF_CHECK_CUDA(cudaStreamSynchronize(d->stream));
   return SF_OK;
@@ -300,6 +317,21 @@ int sf_memcpy_d2h(int dev, void* dst, const void* src, size_t bytes) {
   SF_TRY(ensure_device(dev, &d));
   if (bytes == 0) {
     SF_CHECK_CUDA(cudaStreamSynchronize(d->stream));
+    return SF_OK;
+  }
+  if (bytes >= (64u << 10) && bytes <= (256u << 20)) {
+    // DMA into a pinned bounce buffer at full PCIe/C2C speed, then one memcpy
+    std::lock_guard<std::mutex> lk(d->d2h_mu);
+    if (d->pinned_d2h_bytes < bytes) {
+      if (d->pinned_d2h) cudaFreeHost(d->pinned_d2h);
+      size_t want = 1u << 20;
+      while (want < bytes) want <<= 1;
+      SF_CHECK_CUDA(cudaMallocHost((void**)&d->pinned_d2h, want));
+      d->pinned_d2h_bytes = want;
+    }
+    SF_CHECK_CUDA(cudaMemcpyAsync(d->pinned_d2h, src, bytes, cudaMemcpyDeviceToHost, d->stream));
+    SF_CHECK_CUDA(cudaStreamSynchronize(d->stream));
+    std::memcpy(dst, d->pinned_d2h, bytes);
     return SF_OK;
   }
   SF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, d->stream));
