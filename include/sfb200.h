@@ -115,6 +115,21 @@ int sf_rng(int dev, int kind, int dtype, int64_t n, uint64_t offset, void** out)
 int sf_dropout(int dev, int dtype, int64_t n, const void* x, const void* u, int u_dtype,
                double rate, void** out, void** mask);
 
+/* ------------------------------------------------------- NN plugin kernels
+ * (ResNet-50, configs C4/C5; no reference counterpart — the reference has no
+ * convolution/pooling/xent).  NHWC; g8 = {N, H, W, C, KH, KW,
+ * stride, pad}; output spatial size (H + 2 pad - KH) / stride + 1. */
+int sf_im2col(int dev, int dtype, const int64_t* g8, const void* x, void** cols);
+int sf_col2im(int dev, int dtype, const int64_t* g8, const void* dcols, void** dx);
+int sf_maxpool2d(int dev, int dtype, const int64_t* g8, const void* x, void** y);
+int sf_maxpool2d_grad(int dev, int dtype, const int64_t* g8, const void* x, const void* dy,
+                      void** dx);
+/* per-row softmax cross-entropy with int32 labels, and its gradient scaled by g[row] */
+int sf_softmax_xent(int dev, int dtype, int64_t rows, int64_t k, const void* logits,
+                    const void* labels, void** loss);
+int sf_softmax_xent_grad(int dev, int dtype, int64_t rows, int64_t k, const void* logits,
+                         const void* labels, const void* g, void** out);
+
 /* ------------------------------------------------------- staged graphs */
 /* Compile CUDA C++ source (which may #include "sf_ops.cuh") for sm_100a with
  * NVRTC and load it; returns an opaque kernel handle. Cached by source. */

@@ -67,6 +67,11 @@ def register_all(ref, OpDef, register_op) -> None:
         y = ctx.output(0)
         return [div(ctx.out_grad(), add(y, y))]
 
+    def g_rsqrt(ctx):
+        y = ctx.output(0)
+        half = tensor_from_host([-0.5], (), y.dtype)
+        return [mul(ctx.out_grad(), mul(half, mul(y, mul(y, y))))]
+
     def mask(op, x, y, dt):
         return dispatch("cast", [dispatch(op, [x, y])[0]], {"dtype": dt})[0]
 
@@ -98,7 +103,7 @@ def register_all(ref, OpDef, register_op) -> None:
 
     unary = {"tanh": (np.tanh, g_tanh), "sigmoid": (sigmoid_np, g_sigmoid),
              "square": (lambda x: x * x, g_square), "sqrt": (np.sqrt, g_sqrt),
-             "rsqrt": (lambda x: x.dtype.type(1.0) / np.sqrt(x), None)}
+             "rsqrt": (lambda x: x.dtype.type(1.0) / np.sqrt(x), g_rsqrt)}
     for name, (fn, grad) in unary.items():
         k, inf = f_unary(fn)
         register_op(OpDef(name, 1, {}, 1, False, k, inf, grad, ()))
@@ -142,3 +147,91 @@ def register_all(ref, OpDef, register_op) -> None:
                       uniform_kernel,
                       lambda attrs, s, env=None: [(attrs["dtype"], tuple(attrs["shape"]))],
                       None, ()))
+    register_nn(ref, OpDef, register_op)
+
+
+def register_nn(ref, OpDef, register_op) -> None:
+    """conv2d / max_pool / softmax_xent (and their gradient ops) as numpy
+    plugins, same names/attrs/rules as paper_1903_01855_b200/nn.py."""
+    from stageflow.ops import INT, SHAPE, _schema, dispatch
+
+    from oracle import nn_np
+
+    K = ref.kernels
+
+    def wrap(arr, like, env):
+        return K._wrap(np.ascontiguousarray(arr), like.dtype, env)
+
+    def conv_k(attrs, ins, env):
+        x, w = ins
+        return [wrap(nn_np.conv2d(x.raw(), w.raw(), attrs["stride"], attrs["pad"]), x, env)]
+
+    def conv_i(attrs, in_specs, env=None):
+        (dx, (n, h, w, c)), (_, (kh, kw, ci, co)) = in_specs
+        ho, wo = nn_np.out_hw(h, w, kh, attrs["stride"], attrs["pad"])
+        return [(dx, (n, ho, wo, co))]
+
+    def conv_g(ctx):
+        x, w = ctx.input(0), ctx.input(1)
+        up = ctx.out_grad()
+        a = {"stride": ctx.attrs["stride"], "pad": ctx.attrs["pad"]}
+        gx = dispatch("conv2d_grad_input", [up, w], dict(a, input_shape=tuple(ctx.in_spec(0)[1])))[0]
+        gw = dispatch("conv2d_grad_filter", [x, up],
+                      dict(a, filter_shape=tuple(ctx.in_spec(1)[1])))[0]
+        return [gx, gw]
+
+    def gi_k(attrs, ins, env):
+        dy, w = ins
+        return [wrap(nn_np.conv2d_grad_input(dy.raw(), w.raw(), attrs["stride"], attrs["pad"],
+                                             tuple(attrs["input_shape"])), dy, env)]
+
+    def gf_k(attrs, ins, env):
+        x, dy = ins
+        return [wrap(nn_np.conv2d_grad_filter(x.raw(), dy.raw(), attrs["stride"], attrs["pad"],
+                                              tuple(attrs["filter_shape"])), x, env)]
+
+    def pool_k(attrs, ins, env):
+        (x,) = ins
+        return [wrap(nn_np.max_pool(x.raw(), attrs["ksize"], attrs["stride"], attrs["pad"]), x, env)]
+
+    def pool_i(attrs, in_specs, env=None):
+        dt, (n, h, w, c) = in_specs[0]
+        ho, wo = nn_np.out_hw(h, w, attrs["ksize"], attrs["stride"], attrs["pad"])
+        return [(dt, (n, ho, wo, c))]
+
+    def pool_g(ctx):
+        a = {k: ctx.attrs[k] for k in ("ksize", "stride", "pad")}
+        return [dispatch("max_pool_grad", [ctx.input(0), ctx.out_grad()], a)[0]]
+
+    def pool_gk(attrs, ins, env):
+        x, dy = ins
+        return [wrap(nn_np.max_pool_grad(x.raw(), dy.raw(), attrs["ksize"], attrs["stride"],
+                                         attrs["pad"]), x, env)]
+
+    def xent_k(attrs, ins, env):
+        lg, lab = ins
+        return [wrap(nn_np.softmax_xent(lg.raw(), lab.raw()), lg, env)]
+
+    def xent_g(ctx):
+        return [dispatch("softmax_xent_grad", [ctx.input(0), ctx.input(1), ctx.out_grad()])[0],
+                None]
+
+    def xent_gk(attrs, ins, env):
+        lg, lab, g = ins
+        return [wrap(nn_np.softmax_xent_grad(lg.raw(), lab.raw(), g.raw()), lg, env)]
+
+    same = lambda attrs, s, env=None: [s[0]]  # noqa: E731
+    conv_attrs = _schema(stride=INT, pad=INT)
+    pool_attrs = _schema(ksize=INT, stride=INT, pad=INT)
+    register_op(OpDef("conv2d", 2, conv_attrs, 1, False, conv_k, conv_i, conv_g, ()))
+    register_op(OpDef("conv2d_grad_input", 2, _schema(stride=INT, pad=INT, input_shape=SHAPE), 1,
+                      False, gi_k, lambda attrs, s, env=None: [(s[0][0], tuple(attrs["input_shape"]))],
+                      None, ()))
+    register_op(OpDef("conv2d_grad_filter", 2, _schema(stride=INT, pad=INT, filter_shape=SHAPE),
+                      1, False, gf_k,
+                      lambda attrs, s, env=None: [(s[0][0], tuple(attrs["filter_shape"]))], None, ()))
+    register_op(OpDef("max_pool", 1, pool_attrs, 1, False, pool_k, pool_i, pool_g, ()))
+    register_op(OpDef("max_pool_grad", 2, pool_attrs, 1, False, pool_gk, same, None, ()))
+    register_op(OpDef("softmax_xent", 2, {}, 1, False, xent_k,
+                      lambda attrs, s, env=None: [(s[0][0], (s[0][1][0],))], xent_g, ()))
+    register_op(OpDef("softmax_xent_grad", 3, {}, 1, False, xent_gk, same, None, ()))

@@ -81,6 +81,15 @@ def _declare(lib: ctypes.CDLL) -> None:
                                    ctypes.c_uint64, _PVP]),
         "sf_dropout": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _VP, _VP, ctypes.c_int,
                                        ctypes.c_double, _PVP, _PVP]),
+        "sf_im2col": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP, _PVP]),
+        "sf_col2im": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP, _PVP]),
+        "sf_maxpool2d": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP, _PVP]),
+        "sf_maxpool2d_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP,
+                                              _VP, _PVP]),
+        "sf_softmax_xent": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _I64, _VP, _VP,
+                                            _PVP]),
+        "sf_softmax_xent_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _I64, _VP,
+                                                 _VP, _VP, _PVP]),
         "sf_jit_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _PVP]),
         "sf_jit_log": (ctypes.c_char_p, []),
         "sf_jit_launch": (ctypes.c_int, [ctypes.c_int, _VP, ctypes.c_uint, ctypes.c_uint,
@@ -108,8 +117,19 @@ EXPORTED_SYMBOLS = (
     "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
-    "sf_plan_profile", "sf_plan_step_stats",
+    "sf_plan_profile", "sf_plan_step_stats", "sf_im2col", "sf_col2im", "sf_maxpool2d",
+    "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad",
 )
+
+
+def nn_call(name: str, dev: int, *args, out_nbytes: int) -> "DeviceBuffer":
+    """Call one of the NN entry points whose last argument is `void** out`."""
+    L = require_device()
+    out, ref = _outslot()
+    rc = getattr(L, name)(dev, *args, ref)
+    if rc:
+        raise _err(L, rc, name)
+    return DeviceBuffer(dev, out.value, out_nbytes)
 
 
 def load_library() -> ctypes.CDLL:

@@ -35,8 +35,12 @@ __device__ __forceinline__ T ld_b(const T* b, long long k, long long n, long lon
 template <class T, bool TA, bool TB>
 __global__ void __launch_bounds__(256) gemm_tiled(const T* __restrict__ A, const T* __restrict__ B,
                                                   T* __restrict__ C, long long m, long long n,
-                                                  long long k) {
+                                                  long long k, long long kchunk) {
+  // blockIdx.z selects a k-range (split-K); without a split kchunk == k
   constexpr int BM = 64, BN = 64, BK = 16;
+  const long long kb = (long long)blockIdx.z * kchunk;
+  const long long ke = kb + kchunk < k ? kb + kchunk : k;
+  C += (long long)blockIdx.z * m * n;
   __shared__ T As[BK][BM + 1];
   __shared__ T Bs[BK][BN + 1];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -46,7 +50,7 @@ __global__ void __launch_bounds__(256) gemm_tiled(const T* __restrict__ A, const
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
-  for (long long k0 = 0; k0 < k; k0 += BK) {
+  for (long long k0 = kb; k0 < ke; k0 += BK) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int e = threadIdx.x + t * 256;  // 0..1023
@@ -54,17 +58,17 @@ __global__ void __launch_bounds__(256) gemm_tiled(const T* __restrict__ A, const
       {
         const int mi = e / BK, ki = e % BK;
         const long long gi = row0 + mi, gk = k0 + ki;
-        As[ki][mi] = (gi < m && gk < k) ? ld_a<T, TA, TB>(A, m, k, gi, gk) : T(0);
+        As[ki][mi] = (gi < m && gk < ke) ? ld_a<T, TA, TB>(A, m, k, gi, gk) : T(0);
       }
       // B tile: BK x BN
       {
         const int ki = e / BN, nj = e % BN;
         const long long gk = k0 + ki, gj = col0 + nj;
-        Bs[ki][nj] = (gk < k && gj < n) ? ld_b<T, TA, TB>(B, k, n, gk, gj) : T(0);
+        Bs[ki][nj] = (gk < ke && gj < n) ? ld_b<T, TA, TB>(B, k, n, gk, gj) : T(0);
       }
     }
     __syncthreads();
-    const int kmax = (k - k0) < BK ? (int)(k - k0) : BK;
+    const int kmax = (ke - k0) < BK ? (int)(ke - k0) : BK;
     for (int kk = 0; kk < kmax; ++kk) {
       T av[4], bv[4];
 #pragma unroll
@@ -90,6 +94,17 @@ __global__ void __launch_bounds__(256) gemm_tiled(const T* __restrict__ A, const
   }
 }
 
+// Split-K epilogue: C[i] = sum over splits, in split order (deterministic).
+template <class T>
+__global__ void splitk_sum(const T* __restrict__ W, T* __restrict__ C, long long mn, int splits) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mn; i += stride) {
+    T acc = W[i];
+    for (int s = 1; s < splits; ++s) acc = acc + W[(long long)s * mn + i];
+    C[i] = acc;
+  }
+}
+
 // Small GEMM: one thread per output (k short), same sequential-k FMA order.
 template <class T, bool TA, bool TB>
 __global__ void gemm_small(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
@@ -112,8 +127,34 @@ static void gemm_go(Device* d, const T* A, const T* B, T* C, long long m, long l
     if (blocks < 1) blocks = 1;
     gemm_small<T, TA, TB><<<(unsigned)blocks, 256, 0, d->stream>>>(A, B, C, m, n, k);
   } else {
+    const long long tiles = ((n + 63) / 64) * ((m + 63) / 64);
+    long long splits = 1;
+    // Long contractions over few output tiles (conv weight gradients: k = N*H*W)
+    // are split along k.  Only k >= 16384 splits, so every matmul a fused
+    // staged kernel can inline (k*n <= 1024) keeps the sequential-k order.
+    if (k >= 16384 && tiles < 2LL * d->sm_count) {
+      splits = (2LL * d->sm_count + tiles - 1) / tiles;
+      const long long by_k = k / 4096;
+      if (splits > by_k) splits = by_k;
+      if (splits > 64) splits = 64;
+      if (splits < 1) splits = 1;
+    }
+    if (splits > 1) {
+      const long long kchunk = ((k + splits - 1) / splits + 15) / 16 * 16;
+      splits = (k + kchunk - 1) / kchunk;
+      T* work = nullptr;
+      if (d->alloc.alloc(d->id, sizeof(T) * (size_t)(splits * m * n), (void**)&work) == SF_OK) {
+        dim3 grid((unsigned)((n + 63) / 64), (unsigned)((m + 63) / 64), (unsigned)splits);
+        gemm_tiled<T, TA, TB><<<grid, 256, 0, d->stream>>>(A, B, work, m, n, k, kchunk);
+        long long blocks = (m * n + 255) / 256;
+        if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
+        splitk_sum<T><<<(unsigned)blocks, 256, 0, d->stream>>>(work, C, m * n, (int)splits);
+        d->alloc.release(work);  // stream-ordered reuse is safe
+        return;
+      }
+    }
     dim3 grid((unsigned)((n + 63) / 64), (unsigned)((m + 63) / 64));
-    gemm_tiled<T, TA, TB><<<grid, 256, 0, d->stream>>>(A, B, C, m, n, k);
+    gemm_tiled<T, TA, TB><<<grid, 256, 0, d->stream>>>(A, B, C, m, n, k, k);
   }
 }
 

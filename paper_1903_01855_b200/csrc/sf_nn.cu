@@ -1,0 +1,358 @@
+// sf_nn.cu — kernels behind the ResNet-50 plugin ops (BASELINE configs C4/C5).
+//
+// The reference has no convolution, pooling or cross-entropy;
+// these ops are registered through its own plugin ABI (nn.py).  Layout is
+// NHWC, filters are (KH, KW, Cin, Cout), float32 or float64.
+//
+//   conv2d            = im2col (this file) + the GEMM of sf_matmul.cu
+//   conv2d_grad_input = GEMM (dy @ W^T) + col2im gather (this file)
+//   conv2d_grad_filter= GEMM (cols^T @ dy, split-K for long M)
+//   max_pool / max_pool_grad, softmax_xent / softmax_xent_grad (this file)
+//
+// Every reduction here has a fixed order (gathers instead of atomics), so an
+// op gives identical bits eagerly and inside a staged program.
+#include "sf_internal.h"
+#include "sf_ops.cuh"
+
+namespace sfrt {
+
+struct ConvGeom {
+  long long n, h, w, c, kh, kw, s, p, ho, wo;
+};
+
+static unsigned grid_for_n(Device* d, long long n) {
+  long long b = (n + 255) / 256;
+  const long long cap = (long long)d->sm_count * 32;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// cols[(n, oh, ow), (kh, kw, c)] = x[n, oh*s - p + kh, ow*s - p + kw, c] (0 outside)
+template <class T>
+__global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, ConvGeom g) {
+  const long long K = g.kh * g.kw * g.c;
+  const long long total = g.n * g.ho * g.wo * K;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long k = i % K, m = i / K;
+    const long long c = k % g.c, t = k / g.c;
+    const long long kw = t % g.kw, kh = t / g.kw;
+    const long long ow = m % g.wo, t2 = m / g.wo;
+    const long long oh = t2 % g.ho, n = t2 / g.ho;
+    const long long ih = oh * g.s - g.p + kh, iw = ow * g.s - g.p + kw;
+    T v = T(0);
+    if (ih >= 0 && ih < g.h && iw >= 0 && iw < g.w) v = x[((n * g.h + ih) * g.w + iw) * g.c + c];
+    cols[i] = v;
+  }
+}
+
+// dx[n, h, w, c] = sum over (kh, kw) (fixed order) of dcols[(n, oh, ow), (kh, kw, c)]
+template <class T>
+__global__ void col2im_kernel(const T* __restrict__ dcols, T* __restrict__ dx, ConvGeom g) {
+  const long long K = g.kh * g.kw * g.c;
+  const long long total = g.n * g.h * g.w * g.c;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long c = i % g.c, t = i / g.c;
+    const long long w = t % g.w, t2 = t / g.w;
+    const long long h = t2 % g.h, n = t2 / g.h;
+    T acc = T(0);
+    bool any = false;
+    for (long long kh = 0; kh < g.kh; ++kh) {
+      const long long y = h + g.p - kh;
+      if (y < 0 || y % g.s) continue;
+      const long long oh = y / g.s;
+      if (oh >= g.ho) continue;
+      for (long long kw = 0; kw < g.kw; ++kw) {
+        const long long xx = w + g.p - kw;
+        if (xx < 0 || xx % g.s) continue;
+        const long long ow = xx / g.s;
+        if (ow >= g.wo) continue;
+        const T v = dcols[((n * g.ho + oh) * g.wo + ow) * K + (kh * g.kw + kw) * g.c + c];
+        acc = any ? sf::add(acc, v) : v;
+        any = true;
+      }
+    }
+    dx[i] = acc;
+  }
+}
+
+// max pool, window k x k, stride s, pad p (padding never wins); first max
+// in (kh, kw) order is the argmax used by the gradient.
+template <class T>
+__global__ void maxpool_kernel(const T* __restrict__ x, T* __restrict__ y, ConvGeom g) {
+  const long long total = g.n * g.ho * g.wo * g.c;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long c = i % g.c, t = i / g.c;
+    const long long ow = t % g.wo, t2 = t / g.wo;
+    const long long oh = t2 % g.ho, n = t2 / g.ho;
+    T best = T(0);
+    bool have = false;
+    for (long long kh = 0; kh < g.kh; ++kh) {
+      const long long ih = oh * g.s - g.p + kh;
+      if (ih < 0 || ih >= g.h) continue;
+      for (long long kw = 0; kw < g.kw; ++kw) {
+        const long long iw = ow * g.s - g.p + kw;
+        if (iw < 0 || iw >= g.w) continue;
+        const T v = x[((n * g.h + ih) * g.w + iw) * g.c + c];
+        if (!have || v > best || (v != v && best == best)) best = v;
+        have = true;
+      }
+    }
+    y[i] = best;
+  }
+}
+
+template <class T>
+__device__ __forceinline__ bool is_argmax(const T* x, const ConvGeom& g, long long n, long long oh,
+                                          long long ow, long long c, long long h, long long w) {
+  // recompute the window's first max position and compare with (h, w)
+  T best = T(0);
+  long long bh = -1, bw = -1;
+  for (long long kh = 0; kh < g.kh; ++kh) {
+    const long long ih = oh * g.s - g.p + kh;
+    if (ih < 0 || ih >= g.h) continue;
+    for (long long kw = 0; kw < g.kw; ++kw) {
+      const long long iw = ow * g.s - g.p + kw;
+      if (iw < 0 || iw >= g.w) continue;
+      const T v = x[((n * g.h + ih) * g.w + iw) * g.c + c];
+      if (bh < 0 || v > best || (v != v && best == best)) {
+        best = v;
+        bh = ih;
+        bw = iw;
+      }
+    }
+  }
+  return bh == h && bw == w;
+}
+
+template <class T>
+__global__ void maxpool_grad_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                    T* __restrict__ dx, ConvGeom g) {
+  const long long total = g.n * g.h * g.w * g.c;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long c = i % g.c, t = i / g.c;
+    const long long w = t % g.w, t2 = t / g.w;
+    const long long h = t2 % g.h, n = t2 / g.h;
+    T acc = T(0);
+    bool any = false;
+    for (long long kh = 0; kh < g.kh; ++kh) {
+      const long long y = h + g.p - kh;
+      if (y < 0 || y % g.s) continue;
+      const long long oh = y / g.s;
+      if (oh >= g.ho) continue;
+      for (long long kw = 0; kw < g.kw; ++kw) {
+        const long long xx = w + g.p - kw;
+        if (xx < 0 || xx % g.s) continue;
+        const long long ow = xx / g.s;
+        if (ow >= g.wo) continue;
+        if (!is_argmax(x, g, n, oh, ow, c, h, w)) continue;
+        const T v = dy[((n * g.ho + oh) * g.wo + ow) * g.c + c];
+        acc = any ? sf::add(acc, v) : v;
+        any = true;
+      }
+    }
+    dx[i] = acc;
+  }
+}
+
+// softmax cross-entropy per row: loss = log(sum exp(x - m)) + m - x[label];
+// one warp per row; the sum follows the canonical reduction order.
+template <class T>
+__global__ void xent_kernel(const T* __restrict__ logits, const int* __restrict__ labels,
+                            long long rows, long long k, T* __restrict__ loss) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += warps) {
+    const T* row = logits + r * k;
+    T m = -INFINITY;
+    for (long long j = lane; j < k; j += 32) m = sf::maximum(m, row[j]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = sf::maximum(m, __shfl_xor_sync(0xffffffffu, m, off));
+    T acc = T(0);
+    bool present = false;
+    for (long long j = lane; j < k; j += 32) {
+      const T e = sf::exp_(sf::sub(row[j], m));
+      acc = present ? sf::add(acc, e) : e;
+      present = true;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const T ov = __shfl_xor_sync(0xffffffffu, acc, off);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, off);
+      if (present && op) acc = sf::add(acc, ov);
+      else if (op) acc = ov;
+      present = present || op;
+    }
+    if (lane == 0) {
+      const int lab = labels[r];
+      const T picked = (lab >= 0 && lab < k) ? row[lab] : T(NAN);
+      loss[r] = sf::sub(sf::add(sf::log_(acc), m), picked);
+    }
+  }
+}
+
+// d logits = g[r] * (softmax - onehot(label))
+template <class T>
+__global__ void xent_grad_kernel(const T* __restrict__ logits, const int* __restrict__ labels,
+                                 const T* __restrict__ g, long long rows, long long k,
+                                 T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += warps) {
+    const T* row = logits + r * k;
+    T m = -INFINITY;
+    for (long long j = lane; j < k; j += 32) m = sf::maximum(m, row[j]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = sf::maximum(m, __shfl_xor_sync(0xffffffffu, m, off));
+    T acc = T(0);
+    bool present = false;
+    for (long long j = lane; j < k; j += 32) {
+      const T e = sf::exp_(sf::sub(row[j], m));
+      acc = present ? sf::add(acc, e) : e;
+      present = true;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const T ov = __shfl_xor_sync(0xffffffffu, acc, off);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, off);
+      if (present && op) acc = sf::add(acc, ov);
+      else if (op) acc = ov;
+      present = present || op;
+    }
+    const int lab = labels[r];
+    const T gr = g ? g[r] : T(1);
+    for (long long j = lane; j < k; j += 32) {
+      const T p = sf::div(sf::exp_(sf::sub(row[j], m)), acc);
+      out[r * k + j] = sf::mul(gr, j == lab ? sf::sub(p, T(1)) : p);
+    }
+  }
+}
+
+template <class F>
+static int by_dtype(int dtype, F&& f) {
+  if (dtype == SF_DTYPE_F32) return f(float());
+  if (dtype == SF_DTYPE_F64) return f(double());
+  set_error("nn ops require float tensors");
+  return SF_ERR_INVALID;
+}
+
+}  // namespace sfrt
+
+using namespace sfrt;
+
+static ConvGeom geom(const int64_t* g) {
+  ConvGeom c;
+  c.n = g[0]; c.h = g[1]; c.w = g[2]; c.c = g[3]; c.kh = g[4]; c.kw = g[5]; c.s = g[6]; c.p = g[7];
+  c.ho = (c.h + 2 * c.p - c.kh) / c.s + 1;
+  c.wo = (c.w + 2 * c.p - c.kw) / c.s + 1;
+  return c;
+}
+
+extern "C" {
+
+// g = {N, H, W, C, KH, KW, stride, pad}
+int sf_im2col(int dev, int dtype, const int64_t* g8, const void* x, void** cols) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  const ConvGeom g = geom(g8);
+  const long long total = g.n * g.ho * g.wo * g.kh * g.kw * g.c;
+  if (*cols == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * dtype_size(dtype), cols));
+  if (total == 0) return SF_OK;
+  count_launch(dev);
+  return by_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    im2col_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)x, (T*)*cols, g);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  });
+}
+
+int sf_col2im(int dev, int dtype, const int64_t* g8, const void* dcols, void** dx) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  const ConvGeom g = geom(g8);
+  const long long total = g.n * g.h * g.w * g.c;
+  if (*dx == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * dtype_size(dtype), dx));
+  if (total == 0) return SF_OK;
+  count_launch(dev);
+  return by_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    col2im_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)dcols, (T*)*dx, g);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  });
+}
+
+int sf_maxpool2d(int dev, int dtype, const int64_t* g8, const void* x, void** y) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  const ConvGeom g = geom(g8);
+  const long long total = g.n * g.ho * g.wo * g.c;
+  if (*y == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * dtype_size(dtype), y));
+  if (total == 0) return SF_OK;
+  count_launch(dev);
+  return by_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    maxpool_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)x, (T*)*y, g);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  });
+}
+
+int sf_maxpool2d_grad(int dev, int dtype, const int64_t* g8, const void* x, const void* dy,
+                      void** dx) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  const ConvGeom g = geom(g8);
+  const long long total = g.n * g.h * g.w * g.c;
+  if (*dx == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * dtype_size(dtype), dx));
+  if (total == 0) return SF_OK;
+  count_launch(dev);
+  return by_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    maxpool_grad_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>(
+        (const T*)x, (const T*)dy, (T*)*dx, g);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  });
+}
+
+int sf_softmax_xent(int dev, int dtype, int64_t rows, int64_t k, const void* logits,
+                    const void* labels, void** loss) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*loss == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)rows * dtype_size(dtype), loss));
+  if (rows == 0) return SF_OK;
+  count_launch(dev);
+  return by_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    xent_kernel<T><<<grid_for_n(d, rows * 32), 256, 0, d->stream>>>(
+        (const T*)logits, (const int*)labels, rows, k, (T*)*loss);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  });
+}
+
+int sf_softmax_xent_grad(int dev, int dtype, int64_t rows, int64_t k, const void* logits,
+                         const void* labels, const void* g, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(rows * k) * dtype_size(dtype), out));
+  if (rows == 0) return SF_OK;
+  count_launch(dev);
+  return by_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    xent_grad_kernel<T><<<grid_for_n(d, rows * 32), 256, 0, d->stream>>>(
+        (const T*)logits, (const int*)labels, (const T*)g, rows, k, (T*)*out);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+"""Neural-network plugin ops for ResNet-50 (BASELINE configs C4/C5).
+
+The reference has no convolution, pooling or cross-entropy,
+so, as the survey prescribes, they enter through the reference's own plugin
+API: ``OpDef`` + ``register_op`` (stageflow/ops.py:45-59, :155-157).  Each op
+is a native kernel sequence (csrc/sf_nn.cu + the GEMM of sf_matmul.cu);
+gradients are dispatched ops, so eager tapes and the staged backward
+(backprop.py) both work.  Batch norm, ReLU, residual adds, global average
+pooling and the classifier are composed from built-in primitives by the
+model (workloads/resnet.py).  Layout: NHWC activations, (KH, KW, Cin, Cout)
+filters.
+"""
+from __future__ import annotations
+
+import struct
+from typing import List
+
+from . import _native, dtypes
+from .dtypes import DType
+from .errors import KernelError
+from .kernels import ordinal_of
+from .ops import INT, SHAPE, OpDef, _schema, dispatch, get_runtime
+from .tensor import Tensor
+
+
+def _out_hw(h, w, k, s, p):
+    return (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+
+
+def _geom(n, h, w, c, kh, kw, s, p) -> bytes:
+    return struct.pack("<8q", n, h, w, c, kh, kw, s, p)
+
+
+def _check_float(op, *ts):
+    for t in ts:
+        if not t.dtype.is_float:
+            raise KernelError(f"{op} requires float tensors, got {t.dtype.value}")
+
+
+def _mm(dev, dt: DType, m, n, k, a_ptr, ta, b_ptr, tb):
+    return _native.matmul(dev, dt.tag, m, n, k, a_ptr, ta, b_ptr, tb, m * n * dt.width)
+
+
+# ---------------------------------------------------------------- conv2d
+def _conv_infer(attrs, in_specs, env=None):
+    (dx, xs), (dw, ws) = in_specs
+    if dx is not dw or not dx.is_float:
+        raise KernelError("conv2d requires two float tensors of one dtype")
+    if len(xs) != 4 or len(ws) != 4:
+        raise KernelError("conv2d expects NHWC input and (KH, KW, Cin, Cout) filters")
+    n, h, w, c = xs
+    kh, kw, ci, co = ws
+    if c is not None and ci is not None and c != ci:
+        raise KernelError(f"conv2d: input channels {c} != filter channels {ci}")
+    s, p = attrs["stride"], attrs["pad"]
+    ho, wo = (None, None) if h is None or w is None else _out_hw(h, w, kh, s, p)
+    return [(dx, (n, ho, wo, co))]
+
+
+def _is_pointwise(kh, kw, s, p):
+    return kh == 1 and kw == 1 and s == 1 and p == 0
+
+
+def _conv_kernel(attrs, inputs, env):
+    x, w = inputs
+    _check_float("conv2d", x, w)
+    n, h, wd, c = x.shape
+    kh, kw, ci, co = w.shape
+    if c != ci:
+        raise KernelError(f"conv2d: input channels {c} != filter channels {ci}")
+    s, p = attrs["stride"], attrs["pad"]
+    ho, wo = _out_hw(h, wd, kh, s, p)
+    dev = ordinal_of(env.device)
+    m, k = n * ho * wo, kh * kw * c
+    if _is_pointwise(kh, kw, s, p):
+        out = _mm(dev, x.dtype, m, co, k, x._ptr(), 0, w._ptr(), 0)
+    else:
+        cols = _native.nn_call("sf_im2col", dev, x.dtype.tag, _geom(n, h, wd, c, kh, kw, s, p),
+                               x._ptr(), out_nbytes=m * k * x.dtype.width)
+        out = _mm(dev, x.dtype, m, co, k, cols.ptr, 0, w._ptr(), 0)
+        del cols
+    return [Tensor._adopt(x.dtype, (n, ho, wo, co), env.device, out)]
+
+
+def _conv_grad(ctx):
+    x, w = ctx.input(0), ctx.input(1)
+    up = ctx.out_grad()
+    a = {"stride": ctx.attrs["stride"], "pad": ctx.attrs["pad"]}
+    gx = dispatch("conv2d_grad_input", [up, w], dict(a, input_shape=tuple(ctx.in_spec(0)[1])))[0]
+    gw = dispatch("conv2d_grad_filter", [x, up], dict(a, filter_shape=tuple(ctx.in_spec(1)[1])))[0]
+    return [gx, gw]
+
+
+def _conv_gi_infer(attrs, in_specs, env=None):
+    return [(in_specs[0][0], tuple(attrs["input_shape"]))]
+
+
+def _conv_gi_kernel(attrs, inputs, env):
+    dy, w = inputs
+    n, h, wd, c = attrs["input_shape"]
+    kh, kw, ci, co = w.shape
+    s, p = attrs["stride"], attrs["pad"]
+    ho, wo = _out_hw(h, wd, kh, s, p)
+    dev = ordinal_of(env.device)
+    m, k = n * ho * wo, kh * kw * c
+    dcols = _mm(dev, dy.dtype, m, k, co, dy._ptr(), 0, w._ptr(), 1)  # dy @ W^T
+    if _is_pointwise(kh, kw, s, p):
+        return [Tensor._adopt(dy.dtype, (n, h, wd, c), env.device, dcols)]
+    dx = _native.nn_call("sf_col2im", dev, dy.dtype.tag, _geom(n, h, wd, c, kh, kw, s, p),
+                         dcols.ptr, out_nbytes=n * h * wd * c * dy.dtype.width)
+    del dcols
+    return [Tensor._adopt(dy.dtype, (n, h, wd, c), env.device, dx)]
+
+
+def _conv_gf_infer(attrs, in_specs, env=None):
+    return [(in_specs[0][0], tuple(attrs["filter_shape"]))]
+
+
+def _conv_gf_kernel(attrs, inputs, env):
+    x, dy = inputs
+    n, h, wd, c = x.shape
+    kh, kw, ci, co = attrs["filter_shape"]
+    s, p = attrs["stride"], attrs["pad"]
+    ho, wo = _out_hw(h, wd, kh, s, p)
+    dev = ordinal_of(env.device)
+    m, k = n * ho * wo, kh * kw * c
+    if _is_pointwise(kh, kw, s, p):
+        dw = _mm(dev, x.dtype, k, co, m, x._ptr(), 1, dy._ptr(), 0)  # X^T @ dy
+    else:
+        cols = _native.nn_call("sf_im2col", dev, x.dtype.tag, _geom(n, h, wd, c, kh, kw, s, p),
+                               x._ptr(), out_nbytes=m * k * x.dtype.width)
+        dw = _mm(dev, x.dtype, k, co, m, cols.ptr, 1, dy._ptr(), 0)
+        del cols
+    return [Tensor._adopt(x.dtype, (kh, kw, ci, co), env.device, dw)]
+
+
+# ---------------------------------------------------------------- max pool
+def _pool_infer(attrs, in_specs, env=None):
+    dt, (n, h, w, c) = in_specs[0]
+    k, s, p = attrs["ksize"], attrs["stride"], attrs["pad"]
+    ho, wo = (None, None) if h is None or w is None else _out_hw(h, w, k, s, p)
+    return [(dt, (n, ho, wo, c))]
+
+
+def _pool_kernel(attrs, inputs, env):
+    (x,) = inputs
+    _check_float("max_pool", x)
+    n, h, w, c = x.shape
+    k, s, p = attrs["ksize"], attrs["stride"], attrs["pad"]
+    ho, wo = _out_hw(h, w, k, s, p)
+    y = _native.nn_call("sf_maxpool2d", ordinal_of(env.device), x.dtype.tag,
+                        _geom(n, h, w, c, k, k, s, p), x._ptr(),
+                        out_nbytes=n * ho * wo * c * x.dtype.width)
+    return [Tensor._adopt(x.dtype, (n, ho, wo, c), env.device, y)]
+
+
+def _pool_grad(ctx):
+    a = {k: ctx.attrs[k] for k in ("ksize", "stride", "pad")}
+    return [dispatch("max_pool_grad", [ctx.input(0), ctx.out_grad()], a)[0]]
+
+
+def _pool_grad_kernel(attrs, inputs, env):
+    x, dy = inputs
+    n, h, w, c = x.shape
+    k, s, p = attrs["ksize"], attrs["stride"], attrs["pad"]
+    dx = _native.nn_call("sf_maxpool2d_grad", ordinal_of(env.device), x.dtype.tag,
+                         _geom(n, h, w, c, k, k, s, p), x._ptr(), dy._ptr(),
+                         out_nbytes=x.nbytes)
+    return [Tensor._adopt(x.dtype, x.shape, env.device, dx)]
+
+
+# ---------------------------------------------------------------- softmax xent
+def _xent_infer(attrs, in_specs, env=None):
+    (dt, ls), (lt, lab) = in_specs
+    if not dt.is_float or lt is not DType.int32:
+        raise KernelError("softmax_xent expects float logits and int32 labels")
+    if len(ls) != 2 or len(lab) != 1:
+        raise KernelError("softmax_xent expects (N, K) logits and (N,) labels")
+    return [(dt, (ls[0],))]
+
+
+def _xent_kernel(attrs, inputs, env):
+    logits, labels = inputs
+    rows, k = logits.shape
+    y = _native.nn_call("sf_softmax_xent", ordinal_of(env.device), logits.dtype.tag, rows, k,
+                        logits._ptr(), labels._ptr(), out_nbytes=rows * logits.dtype.width)
+    return [Tensor._adopt(logits.dtype, (rows,), env.device, y)]
+
+
+def _xent_grad(ctx):
+    logits, labels = ctx.input(0), ctx.input(1)
+    return [dispatch("softmax_xent_grad", [logits, labels, ctx.out_grad()])[0], None]
+
+
+def _xent_grad_kernel(attrs, inputs, env):
+    logits, labels, g = inputs
+    rows, k = logits.shape
+    y = _native.nn_call("sf_softmax_xent_grad", ordinal_of(env.device), logits.dtype.tag, rows,
+                        k, logits._ptr(), labels._ptr(), g._ptr(), out_nbytes=logits.nbytes)
+    return [Tensor._adopt(logits.dtype, logits.shape, env.device, y)]
+
+
+def _same_as_first(attrs, in_specs, env=None):
+    return [in_specs[0]]
+
+
+def nn_defs() -> List[OpDef]:
+    conv_attrs = _schema(stride=INT, pad=INT)
+    pool_attrs = _schema(ksize=INT, stride=INT, pad=INT)
+    return [
+        OpDef("conv2d", 2, conv_attrs, 1, False, _conv_kernel, _conv_infer, _conv_grad),
+        OpDef("conv2d_grad_input", 2, _schema(stride=INT, pad=INT, input_shape=SHAPE), 1, False,
+              _conv_gi_kernel, _conv_gi_infer),
+        OpDef("conv2d_grad_filter", 2, _schema(stride=INT, pad=INT, filter_shape=SHAPE), 1,
+              False, _conv_gf_kernel, _conv_gf_infer),
+        OpDef("max_pool", 1, pool_attrs, 1, False, _pool_kernel, _pool_infer, _pool_grad),
+        OpDef("max_pool_grad", 2, pool_attrs, 1, False, _pool_grad_kernel, _same_as_first),
+        OpDef("softmax_xent", 2, {}, 1, False, _xent_kernel, _xent_infer, _xent_grad),
+        OpDef("softmax_xent_grad", 3, {}, 1, False, _xent_grad_kernel, _same_as_first),
+    ]
+
+
+def install() -> None:
+    """Register the NN ops (and the elementwise plugins) with the live runtime."""
+    from . import plugins
+    from .ops import register_op
+
+    plugins.install()
+    reg = get_runtime().registry
+    for d in nn_defs():
+        try:
+            reg.get(d.name)
+        except Exception:
+            register_op(d)
+
+
+def conv2d(x, w, stride=1, pad=0):
+    return dispatch("conv2d", [x, w], {"stride": stride, "pad": pad})[0]
+
+
+def max_pool(x, ksize=3, stride=2, pad=1):
+    return dispatch("max_pool", [x], {"ksize": ksize, "stride": stride, "pad": pad})[0]
+
+
+def softmax_xent(logits, labels):
+    return dispatch("softmax_xent", [logits, labels])[0]

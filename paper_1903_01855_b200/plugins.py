@@ -94,6 +94,15 @@ def _grad_sqrt(ctx):
     return [div(ctx.out_grad(), add(y, y))]
 
 
+def _grad_rsqrt(ctx):
+    # d/dx x^-1/2 = -1/2 * y^3
+    from .ops import mul
+
+    y = ctx.output(0)
+    half = tensor_from_host([-0.5], (), y.dtype)
+    return [mul(ctx.out_grad(), mul(half, mul(y, mul(y, y))))]
+
+
 def _mask(cond_op, x, y, dt):
     return dispatch("cast", [dispatch(cond_op, [x, y])[0]], {"dtype": dt})[0]
 
@@ -187,7 +196,8 @@ def _plugin_defs() -> List[OpDef]:
 
     defs = []
     for name, grad in (("tanh", _grad_tanh), ("sigmoid", _grad_sigmoid),
-                       ("square", _grad_square), ("sqrt", _grad_sqrt), ("rsqrt", None)):
+                       ("square", _grad_square), ("sqrt", _grad_sqrt),
+                       ("rsqrt", _grad_rsqrt)):
         k, inf = _float_unary(name)
         defs.append(OpDef(name, 1, {}, 1, False, k, inf, grad, (), ("ew", name)))
     for name, grad in (("maximum", _grad_minmax(True)), ("minimum", _grad_minmax(False))):

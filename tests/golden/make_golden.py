@@ -138,6 +138,36 @@ def l2hmc_fixtures(out):
                 out[f"l2hmc_trace_count_{b}"] = np.array([pf.trace_count])
 
 
+def resnet_fixtures(out):
+    """ResNet-50 (full widths) at 64x64, batch 4: 3 SGD steps on the reference."""
+    from paper_1903_01855_b200.workloads import resnet
+
+    for tag, dt in (("grad0", ref.float32), ("grad64", ref.float64)):
+        ref.init_runtime(ref.RuntimeOptions(executor_workers=1, seed=0))
+        register_ref_plugins()
+        tr = resnet.ResNetTrain(ref, batch=4, mode="eager", image=64, seed=0, dtype=dt)
+        with ref.Tape() as t:
+            loss = tr.forward_loss(tr.x, tr.labels)
+        grads = t.gradient(loss, tr.model.params)
+        out[f"resnet_{tag}_loss"] = np.array([float(loss)])
+        for i in (0, 1, 2, 3, 10, 100, 159, 160):
+            out[f"resnet_{tag}_{i}"] = grads[i].numpy().ravel()[:4096]  # keep fixtures small
+    ref.init_runtime(ref.RuntimeOptions(executor_workers=1, seed=0))
+    register_ref_plugins()
+    tr = resnet.ResNetTrain(ref, batch=4, mode="staged", image=64, seed=0, dtype=ref.float64)
+    out["resnet_f64_losses"] = np.array([tr.run_iteration() for _ in range(3)])
+    for mode in ("eager", "staged"):
+        ref.init_runtime(ref.RuntimeOptions(executor_workers=1, seed=0))
+        register_ref_plugins()
+        tr = resnet.ResNetTrain(ref, batch=4, mode=mode, image=64, seed=0)
+        out[f"resnet_{mode}_losses"] = np.array([tr.run_iteration() for _ in range(3)])
+        out[f"resnet_{mode}_fc_b"] = tr.model.fc_b.numpy()
+        out[f"resnet_{mode}_stem_w"] = tr.model.stem[0].numpy()[:, :, :, :4]
+        if mode == "staged":
+            out["resnet_trace_counts"] = np.array([tr.forward_loss.trace_count,
+                                                   tr.apply_updates.trace_count])
+
+
 def main():
     out = {}
     leapfrog_fixtures(out)
@@ -145,6 +175,7 @@ def main():
     c2_fixtures(out)
     if "--no-l2hmc" not in sys.argv:
         l2hmc_fixtures(out)
+    resnet_fixtures(out)
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     meta = {"reference": "/root/reference/pkg/src/stageflow", "numpy": np.__version__,
