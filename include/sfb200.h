@@ -121,6 +121,8 @@ int sf_dropout(int dev, int dtype, int64_t n, const void* x, const void* u, int 
  * stride, pad}; output spatial size (H + 2 pad - KH) / stride + 1. */
 int sf_im2col(int dev, int dtype, const int64_t* g8, const void* x, void** cols);
 int sf_col2im(int dev, int dtype, const int64_t* g8, const void* dcols, void** dx);
+/* f32 im2col written directly as 3xTF32 hi/lo parts with K padded to kp */
+int sf_im2col_split(int dev, const int64_t* g8, int64_t kp, const void* x, void** hi, void** lo);
 int sf_maxpool2d(int dev, int dtype, const int64_t* g8, const void* x, void** y);
 int sf_maxpool2d_grad(int dev, int dtype, const int64_t* g8, const void* x, const void* dy,
                       void** dx);
@@ -129,6 +131,16 @@ int sf_softmax_xent(int dev, int dtype, int64_t rows, int64_t k, const void* log
                     const void* labels, void** loss);
 int sf_softmax_xent_grad(int dev, int dtype, int64_t rows, int64_t k, const void* logits,
                          const void* labels, const void* g, void** out);
+
+/* fp32-class GEMM on tcgen05 tensor cores (3xTF32):
+ * C[m,n] = A[m,k] . B[n,k]^T, both operands K-major and pre-split into
+ * hi (TF32-representable) + lo parts; k must be a multiple of 4. */
+int sf_gemm_tf32x3(int dev, int64_t m, int64_t n, int64_t k, const void* a_hi, const void* a_lo,
+                   const void* b_hi, const void* b_lo, void** c);
+/* hi/lo split of an fp32 (rows x cols) matrix; transpose=1 writes the
+ * (cols x ldo) transpose with rows zero-padded to ldo. */
+int sf_split_tf32(int dev, int64_t rows, int64_t cols, int64_t ldo, int transpose, const void* x,
+                  void** hi, void** lo);
 
 /* ------------------------------------------------------- staged graphs */
 /* Compile CUDA C++ source (which may #include "sf_ops.cuh") for sm_100a with

@@ -90,6 +90,11 @@ def _declare(lib: ctypes.CDLL) -> None:
                                             _PVP]),
         "sf_softmax_xent_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _I64, _VP,
                                                  _VP, _VP, _PVP]),
+        "sf_gemm_tf32x3": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _I64, _VP, _VP, _VP, _VP,
+                                           _PVP]),
+        "sf_im2col_split": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _I64, _VP, _PVP, _PVP]),
+        "sf_split_tf32": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _I64, ctypes.c_int, _VP, _PVP,
+                                          _PVP]),
         "sf_jit_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _PVP]),
         "sf_jit_log": (ctypes.c_char_p, []),
         "sf_jit_launch": (ctypes.c_int, [ctypes.c_int, _VP, ctypes.c_uint, ctypes.c_uint,
@@ -118,8 +123,38 @@ EXPORTED_SYMBOLS = (
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
     "sf_plan_profile", "sf_plan_step_stats", "sf_im2col", "sf_col2im", "sf_maxpool2d",
-    "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad",
+    "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad", "sf_gemm_tf32x3",
+    "sf_split_tf32", "sf_im2col_split",
 )
+
+
+def im2col_split(dev: int, geom: bytes, m: int, kp: int, src: int):
+    L = require_device()
+    hi, lo = ctypes.c_void_p(0), ctypes.c_void_p(0)
+    rc = L.sf_im2col_split(dev, geom, kp, src, ctypes.byref(hi), ctypes.byref(lo))
+    if rc:
+        raise _err(L, rc, "sf_im2col_split")
+    return DeviceBuffer(dev, hi.value, m * kp * 4), DeviceBuffer(dev, lo.value, m * kp * 4)
+
+
+def gemm_tf32x3(dev: int, m: int, n: int, k: int, a_hi: int, a_lo: int, b_hi: int,
+                b_lo: int) -> "DeviceBuffer":
+    """C[m,n] = A[m,k] . B[n,k]^T on tcgen05 (3xTF32); operands pre-split."""
+    return nn_call("sf_gemm_tf32x3", dev, m, n, k, a_hi, a_lo, b_hi, b_lo, out_nbytes=m * n * 4)
+
+
+def split_tf32(dev: int, rows: int, cols: int, src: int, transpose: bool = False,
+               ldo: int = 0):
+    """(hi, lo) DeviceBuffers of an fp32 matrix (optionally transposed/padded)."""
+    L = require_device()
+    ldo = ldo or (rows if transpose else cols)
+    hi, lo = ctypes.c_void_p(0), ctypes.c_void_p(0)
+    rc = L.sf_split_tf32(dev, rows, cols, ldo, int(transpose), src, ctypes.byref(hi),
+                         ctypes.byref(lo))
+    if rc:
+        raise _err(L, rc, "sf_split_tf32")
+    n = (cols if transpose else rows) * ldo * 4
+    return DeviceBuffer(dev, hi.value, n), DeviceBuffer(dev, lo.value, n)
 
 
 def nn_call(name: str, dev: int, *args, out_nbytes: int) -> "DeviceBuffer":

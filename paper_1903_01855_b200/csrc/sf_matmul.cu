@@ -121,7 +121,7 @@ __global__ void gemm_small(const T* __restrict__ A, const T* __restrict__ B, T* 
 
 template <class T, bool TA, bool TB>
 static void gemm_go(Device* d, const T* A, const T* B, T* C, long long m, long long n, long long k) {
-  if (m * n <= 4096 || k <= 8) {
+  if ((m * n <= 4096 && k <= 256) || k <= 8) {
     long long blocks = (m * n + 255) / 256;
     if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
     if (blocks < 1) blocks = 1;

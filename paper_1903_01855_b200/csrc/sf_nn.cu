@@ -47,6 +47,30 @@ __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, Con
   }
 }
 
+// im2col fused with the 3xTF32 hi/lo split and K padding (row stride kp):
+// feeds the tcgen05 GEMM directly (csrc/sf_gemm_tc.cu)
+__global__ void im2col_split_kernel(const float* __restrict__ x, float* __restrict__ hi,
+                                    float* __restrict__ lo, ConvGeom g, long long kp) {
+  const long long K = g.kh * g.kw * g.c;
+  const long long total = g.n * g.ho * g.wo * kp;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long k = i % kp, m = i / kp;
+    float v = 0.f;
+    if (k < K) {
+      const long long c = k % g.c, t = k / g.c;
+      const long long kw = t % g.kw, kh = t / g.kw;
+      const long long ow = m % g.wo, t2 = m / g.wo;
+      const long long oh = t2 % g.ho, n = t2 / g.ho;
+      const long long ih = oh * g.s - g.p + kh, iw = ow * g.s - g.p + kw;
+      if (ih >= 0 && ih < g.h && iw >= 0 && iw < g.w) v = x[((n * g.h + ih) * g.w + iw) * g.c + c];
+    }
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
 // dx[n, h, w, c] = sum over (kh, kw) (fixed order) of dcols[(n, oh, ow), (kh, kw, c)]
 template <class T>
 __global__ void col2im_kernel(const T* __restrict__ dcols, T* __restrict__ dx, ConvGeom g) {
@@ -271,6 +295,21 @@ int sf_im2col(int dev, int dtype, const int64_t* g8, const void* x, void** cols)
     SF_CHECK_CUDA(cudaGetLastError());
     return SF_OK;
   });
+}
+
+int sf_im2col_split(int dev, const int64_t* g8, int64_t kp, const void* x, void** hi, void** lo) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  const ConvGeom g = geom(g8);
+  const long long total = g.n * g.ho * g.wo * kp;
+  if (*hi == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * 4, hi));
+  if (*lo == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * 4, lo));
+  if (total == 0) return SF_OK;
+  count_launch(dev);
+  im2col_split_kernel<<<grid_for_n(d, total), 256, 0, d->stream>>>(
+      (const float*)x, (float*)*hi, (float*)*lo, g, kp);
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
 }
 
 int sf_col2im(int dev, int dtype, const int64_t* g8, const void* dcols, void** dx) {

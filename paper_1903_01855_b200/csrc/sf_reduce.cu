@@ -93,6 +93,57 @@ __global__ void reduce_chunks(const RedArgs a, const T* __restrict__ in, A* __re
   }
 }
 
+// Column reduction (x viewed as (R, C), reduce over R, C contiguous): the same
+// CRO per column, but threadIdx.x walks columns so every load is coalesced.
+// Block = 32 columns x 32 partial lanes; partial lane l of column c folds rows
+// l, l+32, ... of the chunk left to right, then the 32 partials of a column
+// are combined with the butterfly tree in shared memory.  Writes one value
+// per (column, chunk) to part[c * n_chunks + chunk].
+template <class T, class A>
+__global__ void __launch_bounds__(1024) reduce_cols(const T* __restrict__ in, long long R,
+                                                    long long C, long long chunk,
+                                                    long long n_chunks, A* __restrict__ part) {
+  __shared__ A acc_s[32][33];
+  __shared__ bool pres_s[32][33];
+  const int tc = threadIdx.x, tl = threadIdx.y;
+  const long long c = (long long)blockIdx.x * 32 + tc;
+  const long long j = blockIdx.y;
+  const long long g0 = j * chunk;
+  long long len = R - g0;
+  if (len > chunk) len = chunk;
+  A acc = A();
+  bool present = false;
+  if (c < C) {
+    for (long long g = tl; g < len; g += 32) {
+      const A v = (A)in[(g0 + g) * C + c];
+      acc = present ? cadd(acc, v) : v;
+      present = true;
+    }
+  }
+  acc_s[tl][tc] = acc;
+  pres_s[tl][tc] = present;
+  __syncthreads();
+  if (tl == 0 && c < C) {
+    A a[32];
+    bool p[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      a[l] = acc_s[l][tc];
+      p[l] = pres_s[l][tc];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+      for (int l = 0; l < off; ++l) {
+        if (p[l] && p[l + off]) a[l] = cadd(a[l], a[l + off]);
+        else if (p[l + off]) a[l] = a[l + off];
+        p[l] = p[l] || p[l + off];
+      }
+    }
+    part[c * n_chunks + j] = a[0];
+  }
+}
+
 // Sequential CRO over <= 32 values per output, one thread per output; used
 // for short reductions (r <= 32) and for the second level over chunk
 // partials.  Identical tree to the warp butterfly above.
@@ -181,6 +232,25 @@ static unsigned grid_cap(Device* d, long long threads) {
 
 template <class T, class A>
 static int run_reduce(Device* d, const RedArgs& a, const T* in, A* sums) {
+  const bool columns = a.kept_nd == 1 && a.kept_stride[0] == 1 && a.red_nd == 1 &&
+                       a.red_stride[0] == a.kept_shape[0] && a.r > 32 && a.n_out >= 8;
+  if (columns) {
+    dim3 grid((unsigned)((a.n_out + 31) / 32), (unsigned)a.n_chunks);
+    if (a.n_chunks == 1) {
+      reduce_cols<T, A><<<grid, dim3(32, 32), 0, d->stream>>>(in, a.r, a.n_out, a.chunk, 1, sums);
+      count_launch(d->id);
+      return SF_OK;
+    }
+    A* part = nullptr;
+    SF_TRY(d->alloc.alloc(d->id, sizeof(A) * a.n_out * a.n_chunks, (void**)&part));
+    reduce_cols<T, A><<<grid, dim3(32, 32), 0, d->stream>>>(in, a.r, a.n_out, a.chunk,
+                                                           a.n_chunks, part);
+    reduce_partials<A><<<grid_cap(d, a.n_out * 32), 256, 0, d->stream>>>(part, a.n_out,
+                                                                        a.n_chunks, sums);
+    count_launch(d->id, 2);
+    d->alloc.release(part);
+    return SF_OK;
+  }
   if (a.r <= 32) {
     reduce_short<T, A><<<grid_cap(d, a.n_out), 256, 0, d->stream>>>(a, in, sums);
     count_launch(d->id);

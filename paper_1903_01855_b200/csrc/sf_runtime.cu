@@ -179,6 +179,7 @@ int sf_init(int* n_devices) {
   SF_TRY(resolve("cuModuleGetFunction", &drv.moduleGetFunction));
   SF_TRY(resolve("cuFuncSetAttribute", &drv.funcSetAttribute));
   SF_TRY(resolve("cuLaunchKernel", &drv.launchKernel));
+  SF_TRY(resolve("cuTensorMapEncodeTiled", &drv.tensorMapEncodeTiled));
   for (int i = 0; i < n && i < 64; ++i) {
     auto d = std::make_unique<Device>();
     d->id = i;

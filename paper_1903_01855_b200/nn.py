@@ -41,6 +41,22 @@ def _mm(dev, dt: DType, m, n, k, a_ptr, ta, b_ptr, tb):
     return _native.matmul(dev, dt.tag, m, n, k, a_ptr, ta, b_ptr, tb, m * n * dt.width)
 
 
+def _ceil4(v: int) -> int:
+    return (v + 3) // 4 * 4
+
+
+def _tc(dev, m, n, k, a_hilo, b_hilo):
+    """C[m,n] = A[m,k] . B[n,k]^T on tcgen05 (3xTF32); a/b given as (hi, lo)."""
+    return _native.gemm_tf32x3(dev, m, n, k, a_hilo[0].ptr, a_hilo[1].ptr, b_hilo[0].ptr,
+                               b_hilo[1].ptr)
+
+
+def _use_tc(dt: DType) -> bool:
+    # float32 convolutions run on the tensor cores (3xTF32, fp32-class error);
+    # float64 keeps the DFMA GEMM.
+    return dt is DType.float32
+
+
 # ---------------------------------------------------------------- conv2d
 def _conv_infer(attrs, in_specs, env=None):
     (dx, xs), (dw, ws) = in_specs
@@ -72,7 +88,16 @@ def _conv_kernel(attrs, inputs, env):
     ho, wo = _out_hw(h, wd, kh, s, p)
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
-    if _is_pointwise(kh, kw, s, p):
+    if _use_tc(x.dtype):
+        kp = _ceil4(k)
+        if _is_pointwise(kh, kw, s, p) and kp == k:
+            a = _native.split_tf32(dev, m, k, x._ptr())
+        else:
+            a = _native.im2col_split(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
+        b = _native.split_tf32(dev, k, co, w._ptr(), transpose=True, ldo=kp)  # W^T, (co, kp)
+        out = _tc(dev, m, co, kp, a, b)
+        del a, b
+    elif _is_pointwise(kh, kw, s, p):
         out = _mm(dev, x.dtype, m, co, k, x._ptr(), 0, w._ptr(), 0)
     else:
         cols = _native.nn_call("sf_im2col", dev, x.dtype.tag, _geom(n, h, wd, c, kh, kw, s, p),
@@ -103,7 +128,13 @@ def _conv_gi_kernel(attrs, inputs, env):
     ho, wo = _out_hw(h, wd, kh, s, p)
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
-    dcols = _mm(dev, dy.dtype, m, k, co, dy._ptr(), 0, w._ptr(), 1)  # dy @ W^T
+    if _use_tc(dy.dtype) and co % 4 == 0:
+        a = _native.split_tf32(dev, m, co, dy._ptr())      # dy, (m, co) K-major
+        b = _native.split_tf32(dev, k, co, w._ptr())       # W as (k, co): B[n=k, k'=co]
+        dcols = _tc(dev, m, k, co, a, b)                   # dy @ W^T
+        del a, b
+    else:
+        dcols = _mm(dev, dy.dtype, m, k, co, dy._ptr(), 0, w._ptr(), 1)  # dy @ W^T
     if _is_pointwise(kh, kw, s, p):
         return [Tensor._adopt(dy.dtype, (n, h, wd, c), env.device, dcols)]
     dx = _native.nn_call("sf_col2im", dev, dy.dtype.tag, _geom(n, h, wd, c, kh, kw, s, p),
@@ -124,7 +155,20 @@ def _conv_gf_kernel(attrs, inputs, env):
     ho, wo = _out_hw(h, wd, kh, s, p)
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
-    if _is_pointwise(kh, kw, s, p):
+    if _use_tc(x.dtype):
+        mp = _ceil4(m)
+        if _is_pointwise(kh, kw, s, p):
+            a = _native.split_tf32(dev, m, c, x._ptr(), transpose=True, ldo=mp)  # X^T (k, mp)
+        else:
+            cols = _native.nn_call("sf_im2col", dev, x.dtype.tag,
+                                   _geom(n, h, wd, c, kh, kw, s, p), x._ptr(),
+                                   out_nbytes=m * k * x.dtype.width)
+            a = _native.split_tf32(dev, m, k, cols.ptr, transpose=True, ldo=mp)  # cols^T
+            del cols
+        b = _native.split_tf32(dev, m, co, dy._ptr(), transpose=True, ldo=mp)    # dy^T (co, mp)
+        dw = _tc(dev, k, co, mp, a, b)
+        del a, b
+    elif _is_pointwise(kh, kw, s, p):
         dw = _mm(dev, x.dtype, k, co, m, x._ptr(), 1, dy._ptr(), 0)  # X^T @ dy
     else:
         cols = _native.nn_call("sf_im2col", dev, x.dtype.tag, _geom(n, h, wd, c, kh, kw, s, p),

@@ -1,0 +1,54 @@
+"""The tcgen05 3xTF32 GEMM (csrc/sf_gemm_tc.cu) against float64 numpy."""
+import numpy as np
+import pytest
+
+import paper_1903_01855_b200 as sf
+from paper_1903_01855_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 128, 32), (256, 128, 64), (200, 96, 36), (1000, 64, 148),
+                                   (5000, 256, 576), (130, 1000, 2048), (33, 7, 4)])
+def test_gemm_tf32x3_vs_float64(m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    b = rng.standard_normal((n, k)).astype(np.float32)
+    ta, tb = sf.constant(a), sf.constant(b)
+    ahi, alo = _native.split_tf32(0, m, k, ta._ptr())
+    bhi, blo = _native.split_tf32(0, n, k, tb._ptr())
+    c = _native.gemm_tf32x3(0, m, n, k, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr)
+    got = _native.download(c, np.float32, (m, n))
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    err = np.abs(got - want).max() / (np.abs(a).max() * np.abs(b).max() * np.sqrt(k))
+    assert err < 1e-5, err
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * np.sqrt(k))
+
+
+@pytest.mark.parametrize("m,n,k", [(512, 64, 576), (300, 128, 147), (1000, 256, 64)])
+def test_gemm_with_transposed_split_b(m, n, k):
+    """C = A @ W with W (k x n) row-major: B = W^T via the transposing split."""
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    kp = (k + 3) // 4 * 4
+    ap = np.zeros((m, kp), np.float32)
+    ap[:, :k] = a
+    ta, tw = sf.constant(ap), sf.constant(w)
+    ahi, alo = _native.split_tf32(0, m, kp, ta._ptr())
+    bhi, blo = _native.split_tf32(0, k, n, tw._ptr(), transpose=True, ldo=kp)
+    c = _native.gemm_tf32x3(0, m, n, kp, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr)
+    got = _native.download(c, np.float32, (m, n))
+    np.testing.assert_allclose(got, a.astype(np.float64) @ w, rtol=1e-4, atol=1e-4 * np.sqrt(k))
+
+
+def test_split_transpose_padding():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((37, 20)).astype(np.float32)
+    tx = sf.constant(x)  # keep the source alive while the kernel reads it
+    hi, lo = _native.split_tf32(0, 37, 20, tx._ptr(), transpose=True, ldo=40)
+    h = _native.download(hi, np.float32, (20, 40))
+    l_ = _native.download(lo, np.float32, (20, 40))
+    np.testing.assert_array_equal(h[:, :37] + l_[:, :37], x.T)
+    assert not np.any(h[:, 37:]) and not np.any(l_[:, 37:])
+    assert np.all((h.view(np.uint32) & 0x1FFF) == 0)

@@ -103,6 +103,16 @@ def test_int32_wraps():
     assert sf.reduce_sum(big).item() == int(np.sum(arr).astype(np.int32))
 
 
+@pytest.mark.parametrize("shape", [(100, 64), (20000, 3 * 64), (50000, 8), (33, 33)])
+def test_column_reduction_matches_row_reduction_bitwise(shape):
+    """The coalesced column kernel and the warp kernel implement one order (CRO)."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal(shape).astype(np.float32)
+    cols = sf.reduce_sum(sf.constant(x), axes=(0,)).numpy()
+    rows = sf.reduce_sum(sf.constant(np.ascontiguousarray(x.T)), axes=(1,)).numpy()
+    assert cols.tobytes() == rows.tobytes()
+
+
 def test_int32_mean_truncates_eagerly():
     t = sf.tensor_from_host([7, 0, 0], (3,), sf.int32)
     assert sf.reduce_mean(t).item() == 2
