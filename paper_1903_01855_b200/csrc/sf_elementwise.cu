@@ -64,6 +64,22 @@ __global__ void ew_strided(const EwArgs a, O* __restrict__ out) {
   }
 }
 
+// Two collapsed dims, < 2^31 elements (row/column broadcasts, e.g. NHWC
+// activations against per-channel vectors): 32-bit index math only.
+template <class T, class O>
+__global__ void ew_2d(const EwArgs a, O* __restrict__ out) {
+  const unsigned n = (unsigned)a.n, cols = (unsigned)a.shape[1];
+  const unsigned stride = gridDim.x * blockDim.x;
+  const unsigned s00 = (unsigned)a.strides[0][0], s01 = (unsigned)a.strides[0][1];
+  const unsigned s10 = (unsigned)a.strides[1][0], s11 = (unsigned)a.strides[1][1];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned r = i / cols, c = i - r * cols;
+    const T x = fetch<T>(a, 0, (long long)(r * s00 + c * s01));
+    const T y = a.n_in > 1 ? fetch<T>(a, 1, (long long)(r * s10 + c * s11)) : x;
+    out[i] = apply<T, O>(a.op, x, y);
+  }
+}
+
 // Flat path: every operand is either full-size contiguous or a scalar.
 template <class T, class O>
 __global__ void ew_flat(const EwArgs a, O* __restrict__ out) {
@@ -196,6 +212,9 @@ template <class T, class O>
 static void dispatch_ew(Device* d, const EwArgs& a, void* out, bool flat) {
   if (flat) {
     ew_flat<T, O><<<grid_for(d, a.n), 256, 0, d->stream>>>(a, (O*)out);
+  } else if (a.ndim == 2 && a.n < (1LL << 31) &&
+             a.shape[0] * (a.strides[0][0] + a.strides[1][0] + 1) < (1LL << 31)) {
+    ew_2d<T, O><<<grid_for(d, a.n), 256, 0, d->stream>>>(a, (O*)out);
   } else {
     ew_strided<T, O><<<grid_for(d, a.n), 256, 0, d->stream>>>(a, (O*)out);
   }

@@ -231,7 +231,7 @@ SF_DEVFN bool compare_f(int op, T a, T b) {
 // SF_CRO_CHUNK-element chunk with the CRO, then reduce the chunk results
 // with the CRO.  NumPy itself sums pairwise; the reference-vs-GPU contract
 // for floats is therefore rtol-based (SURVEY.md §7 hard part (i)).
-#define SF_CRO_CHUNK 8192
+#define SF_CRO_CHUNK 1024
 
 // ------------------------------------------------------------------ RNG
 // Philox4x32-10, counter-based: element i of a draw with (seed, offset)

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(1024) reduce_cols(const T* __restrict__ in, lo
   A acc = A();
   bool present = false;
   if (c < C) {
+#pragma unroll 8
     for (long long g = tl; g < len; g += 32) {
       const A v = (A)in[(g0 + g) * C + c];
       acc = present ? cadd(acc, v) : v;
