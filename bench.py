@@ -380,7 +380,57 @@ def extras(sf, np, _native, plugins, l2hmc):
         c2[mode] = {"ops_per_sec": 300 / dt, "us_per_op": dt * 1e6 / 300}
     c2["staged_over_eager"] = c2["staged"]["ops_per_sec"] / c2["eager"]["ops_per_sec"]
     out["c2_microbench"] = c2
+    out["c4_resnet50_b32"] = resnet_extra(sf, np, _native)
     return out
+
+
+def resnet_extra(sf, np, _native):
+    """C4: ResNet-50 v1.5 train step, batch 32, 224x224 synthetic fp32, 1 GPU."""
+    import torch
+
+    from paper_1903_01855_b200 import nn
+    from paper_1903_01855_b200.workloads import resnet
+
+    row = {}
+    for mode, n in (("staged", 5), ("eager", 3)):
+        sf.init_runtime(sf.RuntimeOptions())
+        nn.install()
+        tr = resnet.ResNetTrain(sf, batch=32, mode=mode, image=224, seed=0)
+        dt = _time_steps(tr.step, n, _native)
+        row[mode] = {"img_per_sec": 32 / dt, "ms_per_step": dt * 1e3,
+                     "useful_tflops": 0.785 / dt}
+        del tr
+    row["staged_over_eager"] = row["staged"]["img_per_sec"] / row["eager"]["img_per_sec"]
+    # roofline of the dominant tensor kernel: the tcgen05 3xTF32 GEMM at the
+    # shape of layer1's 3x3 convolution (M = 32*56*56, N = 64, K = 576),
+    # timed back to back with CUDA events on the backend stream
+    peaks, kind = _peaks()
+    m, n, k = 32 * 56 * 56, 64, 576
+    a = sf.constant(np.random.default_rng(0).standard_normal((m, k)).astype(np.float32))
+    b = sf.constant(np.random.default_rng(1).standard_normal((n, k)).astype(np.float32))
+    ahi, alo = _native.split_tf32(0, m, k, a._ptr())
+    bhi, blo = _native.split_tf32(0, n, k, b._ptr())
+    stream = torch.cuda.ExternalStream(_native.stream_of(0))
+    for _ in range(3):
+        _native.gemm_tf32x3(0, m, n, k, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record(stream)
+    for _ in range(reps):
+        _native.gemm_tf32x3(0, m, n, k, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr)
+    e1.record(stream)
+    _native.sync(0)
+    ms = e0.elapsed_time(e1) / reps
+    useful = 2.0 * m * n * k / (ms * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", 1590.0)
+    row["roofline"] = {"kernel": "gemm_tc_kernel (tcgen05 kind::tf32, 3 passes)",
+                       "shape_mnk": [m, n, k], "ms": ms, "bound": "tensor",
+                       "achieved": useful, "unit": "TFLOP/s (useful fp32 MACs x2)",
+                       "peak": peak, "frac": useful / peak,
+                       "tensor_issue_tflops": 3 * useful,
+                       "peak_kind": f"{kind} bf16 dense (TF32 is half of it; 3xTF32 issues "
+                                    "3 MMAs per useful MAC)"}
+    return row
 
 
 def main():
