@@ -278,4 +278,50 @@ SF_DEVFN double normal_f64(unsigned long long ctr, unsigned long long seed) {
   return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
+// asynchronous global -> shared copy of one 4- or 8-byte element (LDGSTS):
+// a row program's uniform operands are all put in flight at once instead of
+// one dependent load/store pair per operand; sf::cp_wait() before the barrier.
+template <int BYTES>
+SF_DEVFN void cp_async(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(BYTES)
+               : "memory");
+}
+SF_DEVFN void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Volatile shared-memory reads of staged uniform operands.  A row program
+// reads the same weights once per network evaluation; plain loads let ptxas
+// merge every repeat into one register live across the whole chunk (hundreds
+// of weights -> 255 registers + spills, 2 CTAs/SM).  Volatile loads are
+// issued where they are used; the v4/v2 forms fetch a matvec weight row.
+SF_DEVFN unsigned saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+SF_DEVFN float lds(const float* p) {
+  float v;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr(p)));
+  return v;
+}
+SF_DEVFN double lds(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(saddr(p)));
+  return v;
+}
+SF_DEVFN int lds(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(saddr(p)));
+  return v;
+}
+SF_DEVFN bool lds(const bool* p) { return *(const volatile bool*)p; }
+SF_DEVFN float4 lds4(const float* p) {
+  float4 v;
+  asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(saddr(p)));
+  return v;
+}
+SF_DEVFN double2 lds2(const double* p) {
+  double2 v;
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(saddr(p)));
+  return v;
+}
+
 }  // namespace sf

@@ -38,9 +38,13 @@ MIN_BATCH = 2
 # program is cut into chunks of about this many scalar operations; each
 # chunk is its own kernel (rowed values crossing a cut round-trip through
 # L2-resident temporaries) and the chunks compile in parallel.
-CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "1200"))
-# CTAs of 128 threads that must fit per SM (register budget = 64K / (128 * MIN_BLOCKS))
-MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "2"))
+# (B200 sweep, tools/sweep_rows.sh, L2HMC 1e5 chains: 1200 -> 0.38 ms/step,
+# 4800 -> 0.29 ms, 9600 -> 0.28 ms but 3x the compile time, 19200+ slower.)
+CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "4800"))
+# CTAs of 128 threads that must fit per SM (register budget = 64K / (128 *
+# MIN_BLOCKS)); 0 = no minimum, ptxas picks (best in the sweep once the
+# weights are read with volatile vector loads: ~96 registers, no spills)
+MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
 
 
 class RowProgram:
@@ -273,6 +277,35 @@ class _Gen:
         self.rng_ops: List[Tuple[LOp, int]] = []   # (op, count)
         self.outs: List[LV] = []
         self.tmp = 0
+        # staged weights of rowed matvecs get a padded [K, Np] shared layout
+        # (Np = N rounded up to one 16-byte vector) so a weight row is one or
+        # a few vector loads: root id -> (N, Np)
+        self.pad: Dict[int, Tuple[int, int]] = {}
+        self.smem_name: Dict[int, str] = {}
+        if not rp.uniform_only:
+            seen: Dict[int, object] = {}
+            for op in rp.ops:
+                if op.kind != "matmul" or planner.layout_of(op.outs[0])[0] != ROW:
+                    continue
+                b = op.ins[1]
+                r = b.root()
+                if planner.layout_of(b)[0] == ROW or id(r) in self.produced:
+                    continue
+                if r.kind == "const" and r.imm is not None:
+                    continue
+                n = b.shape[1]
+                prev = seen.get(id(r))
+                seen[id(r)] = n if prev in (None, n) else False
+            for rid, n in seen.items():
+                if n is False:
+                    continue
+                width = next(o.ins[1].root().dtype.width for o in rp.ops
+                             if o.kind == "matmul" and id(o.ins[1].root()) == rid)
+                if width not in (4, 8):
+                    continue
+                vw = 16 // width
+                # N dividing the vector: rows pack densely (one load spans rows)
+                self.pad[rid] = (n, n if vw % n == 0 else -(-n // vw) * vw)
 
     # -- operand access -------------------------------------------------------------
     def _input(self, x: LV) -> None:
@@ -301,10 +334,23 @@ class _Gen:
         else:
             self.ext_kind.append(UNI)
             n = r.numel
-            self.smem.append(f"  __shared__ __align__(16) {ct} s{k}[{max(1, n)}];\n"
-                             f"  for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
-                             f"s{k}[q] = ((const {ct}*)a.p[{k}])[q];")
-            self.uni_names[id(r)] = [f"s{k}[{q}]" for q in range(n)]
+            width = r.dtype.width
+            src_q = f"((const {ct}*)a.p[{k}])[q]"
+            if id(r) in self.pad:
+                N, Np = self.pad[id(r)]
+                dst = f"s{k}[(q / {N}) * {Np} + q % {N}]"
+                pidx = [(q // N) * Np + q % N for q in range(n)]
+                size = (n // N) * Np
+            else:
+                dst, pidx, size = f"s{k}[q]", list(range(n)), n
+            copy = (f"sf::cp_async<{width}>(&{dst}, &{src_q});" if width in (4, 8)
+                    else f"{dst} = {src_q};")
+            head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= 128 else
+                    f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) ")
+            self.smem.append(f"  __shared__ __align__(16) {ct} s{k}[{max(1, size)}];\n"
+                             f"  {head}{copy}")
+            self.uni_names[id(r)] = [f"sf::lds(&s{k}[{p}])" for p in pidx]
+            self.smem_name[id(r)] = f"s{k}"
 
     def uni_elem(self, x: LV, flat: int) -> str:
         r = x.root()
@@ -478,11 +524,36 @@ class _Gen:
             # weight loads with other uses of the same weights (which would pin
             # hundreds of weights in registers for the whole chunk)
             lines.append('asm volatile("" ::: "memory");')
-            for j in range(n):
-                acc = f"({ct})0"
+            br = b.root()
+            if id(br) in self.pad:
+                # k-outer: weight row k arrives in 16-byte vector loads and the
+                # n accumulators advance together (same sequential-k FMA chain
+                # per output as the nested form / the eager kernel)
+                N, Np = self.pad[id(br)]
+                sname = self.smem_name[id(br)]
+                vw = 16 // br.dtype.width
+                vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
+                comp = "xyzw"
+                lines.append(" ".join(f"{ct} {nm} = ({ct})0;" for nm in names))
+                vecs: Dict[int, str] = {}   # vector index -> temp (short-lived)
                 for kk in range(kk_n):
-                    acc = f"{fma}({xs[kk]}, {self.uni_elem(b, kk * n + j)}, {acc})"
-                lines.append(f"const {ct} {names[j]} = {acc};")
+                    stmt = []
+                    for c in range(n):
+                        f = kk * Np + c
+                        v = f // vw
+                        if v not in vecs:
+                            t = self._new_tmp()
+                            stmt.append(f"const {vt} {t} = {ld}(&{sname}[{v * vw}]);")
+                            vecs[v] = t
+                        stmt.append(f"{names[c]} = {fma}({xs[kk]}, {vecs[v]}.{comp[f % vw]}, "
+                                    f"{names[c]});")
+                    lines.append(" ".join(stmt))
+            else:
+                for j in range(n):
+                    acc = f"({ct})0"
+                    for kk in range(kk_n):
+                        acc = f"{fma}({xs[kk]}, {self.uni_elem(b, kk * n + j)}, {acc})"
+                    lines.append(f"const {ct} {names[j]} = {acc};")
         elif k == "reduce":
             x = op.ins[0]
             xw = self.P.layout_of(x)[1]
@@ -552,11 +623,11 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
            f"extern \"C\" __global__ void __launch_bounds__("
            f"{'128' if MIN_BLOCKS == 0 else f'128, {MIN_BLOCKS}'}) KNAME(const "
            "__grid_constant__ Params a) {"]
-    decls = [x for x in g.smem if "for (int q" not in x]
-    loads = [x for x in g.smem if "for (int q" in x]
+    loads = [x for x in g.smem if "int q" in x]
+    decls = [x for x in g.smem if "int q" not in x]
     src += decls + loads
     if loads:
-        src.append("  __syncthreads();")
+        src.append("  sf::cp_wait();\n  __syncthreads();")
     src += g.prologue
     if g.prologue:
         src.append("  __syncthreads();")
