@@ -116,7 +116,8 @@ class Program:
         self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)
         from .rowfuse import plan_rows
 
-        units = fuse(plan_rows(lw.ops) if fuse_enabled else lw.ops, fuse_enabled)
+        keep = frozenset(id(v.root()) for v in self.out_vals)
+        units = fuse(plan_rows(lw.ops, keep) if fuse_enabled else lw.ops, fuse_enabled)
         self.segments = self._segment(units)
         self.n_launches = sum(s.n_launches for s in self.segments
                               if isinstance(s, _NativeSegment))

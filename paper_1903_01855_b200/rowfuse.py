@@ -31,6 +31,7 @@ ROW_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "rng", "eye"))
 MAX_UNIFORM_NUMEL = 1024       # uniform values computed per thread
 MAX_MATVEC = 1024              # k*n of a row matmul
 MAX_SMEM_BYTES = 40 * 1024     # uniform inputs staged in shared memory
+UNIFORM_SMEM_BYTES = 46 * 1024  # uniform kernel: results + staged operands (static smem)
 MIN_BATCH = 2
 
 
@@ -45,6 +46,8 @@ CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "4800"))
 # MIN_BLOCKS)); 0 = no minimum, ptxas picks (best in the sweep once the
 # weights are read with volatile vector loads: ~96 registers, no spills)
 MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
+# re-roll repeated blocks of row ops into loops (LoopOp)
+REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 
 class RowProgram:
@@ -57,7 +60,228 @@ class RowProgram:
         self.uniform_only = False  # single-CTA kernel for chain-independent ops
 
 
-def _op_cost(op: LOp, planner) -> int:
+class LoopOp:
+    """``m`` consecutive, structurally identical blocks of row ops run as one loop.
+
+    Tracing unrolls the sampler's Python loop (the reference traces every
+    leapfrog step into the graph, stageflow/staging.py), so a row program
+    repeats the same block of ops once per step; straight-line code for all
+    of them overflows the SM instruction cache (ncu: ``no_instruction`` was
+    the top stall, and a cold L2 re-fetches every byte of it from HBM).  The
+    blocks are re-rolled into one loop body: rowed values flowing from block
+    i-1 into block i become loop-carried registers, per-step uniform operands
+    (time encodings, per-step weights) are stacked in shared memory and
+    indexed by the iteration, and the last block's values used afterwards
+    are exported.  Every element still goes through the identical sequence
+    of scalar operations, so results are bit-for-bit those of the unrolled
+    code.
+    """
+
+    __slots__ = ("kind", "name", "ins", "outs", "attrs", "body", "m", "carried", "stacked",
+                 "exports")
+
+    def __init__(self):
+        self.kind = "loop"
+        self.name = "loop"
+        self.attrs = {}
+        self.body: List[LOp] = []
+        self.m = 0
+        self.carried: List[Tuple[LV, LV, LV]] = []    # (synthetic, init value, body source)
+        self.stacked: List[Tuple[LV, List[LV]]] = []  # (synthetic, per-iteration roots)
+        self.exports: List[Tuple[LV, LV]] = []        # (last block's value, body value)
+        self.ins: List[LV] = []
+        self.outs: List[LV] = []
+
+
+_SYN_ID = [1 << 40]
+
+
+def _synthetic(dtype, shape, kind: str, base: Optional[LV] = None) -> LV:
+    _SYN_ID[0] += 1
+    v = LV(_SYN_ID[0], dtype, shape, kind)
+    v.base = base
+    return v
+
+
+MIN_REPS = 3
+MIN_PERIOD = 4
+
+
+def _sig(op: LOp, planner) -> tuple:
+    ins = []
+    for x in op.ins:
+        r = x.root()
+        imm = repr(r.imm) if (r.kind == "const" and r.imm is not None) else None
+        ins.append((tuple(x.shape), x.dtype.value, planner.layout_of(x)[0], imm))
+    return (op.kind, op.name, repr(sorted(op.attrs.items())), tuple(ins),
+            tuple((tuple(o.shape), o.dtype.value) for o in op.outs))
+
+
+def reroll(ops: List[LOp], planner, users: Dict[int, List[LOp]], keep: set) -> List:
+    """Replace tandem repeats of row-op blocks by LoopOps (recursively on the
+    remaining prefix and suffix)."""
+    import numpy as np
+
+    n = len(ops)
+    if n < MIN_PERIOD * MIN_REPS or any(op.kind == "loop" for op in ops):
+        return list(ops)
+    table: Dict[tuple, int] = {}
+    seq = np.array([table.setdefault(_sig(op, planner), len(table)) for op in ops])
+    cands = []
+    for p in range(MIN_PERIOD, n // MIN_REPS + 1):
+        eq = seq[:-p] == seq[p:]
+        cs = np.concatenate(([0], np.cumsum(eq)))
+        last = n - 2 * p
+        if last < 0:
+            break
+        starts = np.arange(last + 1)
+        good = (cs[starts + p] - cs[starts]) == p
+        for s in np.nonzero(good)[0].tolist():
+            if s >= p and good[s - p]:
+                continue  # not the start of a chain
+            reps = 1
+            while s + (reps - 1) * p <= last and good[s + (reps - 1) * p]:
+                reps += 1
+            if reps >= MIN_REPS:
+                cands.append(((reps - 1) * p, p, s, reps))
+    cands.sort(key=lambda c: (-c[0], c[1]))
+    for _score, p, s, reps in cands[:40]:
+        for front in range(3):
+            for back in range(3):
+                m = reps - front - back
+                if m < MIN_REPS:
+                    continue
+                s0 = s + front * p
+                loop = _make_loop(ops[s0:s0 + m * p], p, m, planner, users, keep)
+                if loop is not None:
+                    return (reroll(ops[:s0], planner, users, keep) + [loop]
+                            + reroll(ops[s0 + m * p:], planner, users, keep))
+    return list(ops)
+
+
+def _make_loop(span: List[LOp], p: int, m: int, planner, users, keep) -> Optional[LoopOp]:
+    blocks = [span[i * p:(i + 1) * p] for i in range(m)]
+    if any(op.kind == "rng" for op in blocks[0]):
+        return None
+    pos: Dict[int, Tuple[int, int, int]] = {}
+    for i, blk in enumerate(blocks):
+        for j, op in enumerate(blk):
+            for oi, o in enumerate(op.outs):
+                pos[id(o)] = (i, j, oi)
+    in_span = {id(op) for op in span}
+    # values of blocks 1..m-1 may only feed their own block or the next one;
+    # the last block's values used after the loop are exported
+    exports: Dict[int, Tuple[LV, LV]] = {}
+    for i, blk in enumerate(blocks):
+        for j, op in enumerate(blk):
+            for oi, o in enumerate(op.outs):
+                outside = id(o) in keep or any(id(u) not in in_span
+                                               for u in users.get(id(o), ()))
+                if i < m - 1:
+                    if outside:
+                        return None
+                elif outside:
+                    exports[id(o)] = (o, blocks[0][j].outs[oi])
+    # per-op block index of every user inside the span (for the i/i+1 rule)
+    block_of = {}
+    for i, blk in enumerate(blocks):
+        for op in blk:
+            block_of[id(op)] = i
+    for o_id, (i, j, oi) in pos.items():
+        for u in users.get(o_id, ()):
+            bi = block_of.get(id(u))
+            if bi is not None and bi not in (i, i + 1):
+                return None
+    loop = LoopOp()
+    loop.m = m
+    carried: Dict[Tuple[int, int], LV] = {}   # (j', oi) of the source -> synthetic
+    stacked: Dict[tuple, LV] = {}
+    ext: Dict[int, LV] = {}
+    body: List[LOp] = []
+    for j, op0 in enumerate(blocks[0]):
+        new_ins = []
+        for q, x0 in enumerate(op0.ins):
+            xs = [blocks[i][j].ins[q] for i in range(m)]
+            roots = [x.root() for x in xs]
+            r0 = roots[0]
+            if r0.kind == "const" and r0.imm is not None:
+                new_ins.append(x0)  # same literal in every block (part of the signature)
+                continue
+            P = [pos.get(id(r)) for r in roots]
+            L = planner.layout_of(x0)
+            if L[0] == UNI:
+                if any(pp is not None for pp in P):
+                    return None
+                if all(r is r0 for r in roots):
+                    ext[id(r0)] = r0
+                    new_ins.append(x0)
+                    continue
+                if any(x is not r for x, r in zip(xs, roots)) or \
+                        any(r.shape != r0.shape or r.dtype != r0.dtype for r in roots):
+                    return None
+                key = tuple(id(r) for r in roots)
+                syn = stacked.get(key)
+                if syn is None:
+                    syn = _synthetic(r0.dtype, r0.shape, "stacked")
+                    planner.layout[id(syn)] = (UNI,)
+                    stacked[key] = syn
+                    loop.stacked.append((syn, roots))
+                    for r in roots:
+                        ext[id(r)] = r
+                new_ins.append(syn)
+                continue
+            # rowed operand
+            if all(pp is not None and pp[0] == i for i, pp in enumerate(P)):
+                if any(pp[1:] != P[0][1:] for pp in P):
+                    return None
+                new_ins.append(x0)                      # internal to the block
+                continue
+            if all(pp is None for pp in P):
+                if any(r is not r0 for r in roots):
+                    return None
+                ext[id(r0)] = r0
+                new_ins.append(x0)                      # loop-invariant
+                continue
+            if P[0] is None and all(pp is not None and pp[0] == i - 1
+                                    for i, pp in enumerate(P) if i):
+                src = P[1][1:]
+                if any(pp[1:] != src for pp in P[1:]):
+                    return None
+                if any(x.shape != xs[0].shape for x in xs):
+                    return None
+                syn = carried.get(src)
+                if syn is None:
+                    syn = _synthetic(r0.dtype, r0.shape, "carried")
+                    planner.layout[id(syn)] = planner.layout_of(r0)
+                    carried[src] = syn
+                    body_src = blocks[0][src[0]].outs[src[1]]
+                    if body_src.shape != r0.shape or body_src.dtype != r0.dtype:
+                        return None
+                    loop.carried.append((syn, r0, body_src))
+                    ext[id(r0)] = r0
+                elif any(c[1] is not r0 for c in loop.carried if c[0] is syn):
+                    return None
+                if x0 is r0:
+                    new_ins.append(syn)
+                else:
+                    al = _synthetic(x0.dtype, x0.shape, "alias", base=syn)
+                    if planner.layout_of(al)[0] == BAD:
+                        return None
+                    new_ins.append(al)
+                continue
+            return None
+        body.append(LOp(op0.kind, op0.name, new_ins, op0.outs, op0.attrs, op0.node_idx,
+                        op0.op_def))
+    loop.body = body
+    loop.exports = list(exports.values())
+    loop.ins = list(ext.values())
+    loop.outs = [e for e, _ in loop.exports]
+    return loop
+
+
+def _op_cost(op, planner) -> int:
+    if op.kind == "loop":
+        return sum(_op_cost(b, planner) for b in op.body)
     o = op.outs[0]
     L = planner.layout_of(o)
     width = L[1] if L[0] == ROW else max(1, o.numel)
@@ -185,9 +409,15 @@ def choose_batch(ops: List[LOp]) -> int:
     return max(counts.items(), key=lambda kv: (kv[1], kv[0]))[0]
 
 
-def plan_rows(ops: List[LOp]) -> List:
-    """Split ops into RowPrograms (runs of row-local ops) and plain ops."""
+def plan_rows(ops: List[LOp], keep=frozenset()) -> List:
+    """Split ops into RowPrograms (runs of row-local ops) and plain ops.
+
+    ``keep``: ids of root values the caller needs afterwards (graph outputs)."""
     batch = choose_batch(ops)
+    users: Dict[int, List[LOp]] = {}
+    for op in ops:
+        for x in op.ins:
+            users.setdefault(id(x.root()), []).append(op)
     # no batch dimension (e.g. the C2 chain on (1, 16)): every value is uniform
     # and runs of small ops become one-warp uniform kernels
     planner = RowPlanner(batch if batch >= MIN_BATCH else -1)
@@ -217,7 +447,7 @@ def plan_rows(ops: List[LOp]) -> List:
                 uni.ops = [op for op in u.ops if planner.layout_of(op.outs[0])[0] != ROW]
                 uni.uniform_only = True
                 body = RowProgram(u.batch)
-                body.ops = row_ops
+                body.ops = reroll(row_ops, planner, users, keep) if REROLL else row_ops
                 chunks = _split(body, planner)
                 if (all(_smem_bytes(c, planner) <= MAX_SMEM_BYTES for c in chunks)
                         and _uniform_smem(uni) <= MAX_SMEM_BYTES):
@@ -264,7 +494,9 @@ class _Gen:
         self.rp = rp
         self.P = planner
         self.needed = needed
+        flat = [b for op in rp.ops for b in (op.body if op.kind == "loop" else (op,))]
         self.produced = {id(o) for op in rp.ops for o in op.outs}
+        self.produced |= {id(o) for op in flat for o in op.outs}
         self.ext: List[LV] = []          # root LVs in pointer order (inputs)
         self.ext_kind: List[str] = []    # "row" | "uni"
         self.ptr_of: Dict[int, int] = {}
@@ -281,10 +513,17 @@ class _Gen:
         # (Np = N rounded up to one 16-byte vector) so a weight row is one or
         # a few vector loads: root id -> (N, Np)
         self.pad: Dict[int, Tuple[int, int]] = {}
-        self.smem_name: Dict[int, str] = {}
+        # root id -> (shared array, base-offset expression) of staged operands
+        self.smem_name: Dict[int, Tuple[str, str]] = {}
+        # uniform kernel: staged global operands, CSE table, aliased results
+        self.staged: Dict[int, str] = {}
+        self.uni_smem = _uniform_smem(rp) if rp.uniform_only else 0
+        self.cse: Dict[tuple, LV] = {}
+        self.alias: Dict[int, LV] = {}
         if not rp.uniform_only:
             seen: Dict[int, object] = {}
-            for op in rp.ops:
+            widths: Dict[int, int] = {}
+            for op in flat:
                 if op.kind != "matmul" or planner.layout_of(op.outs[0])[0] != ROW:
                     continue
                 b = op.ins[1]
@@ -296,12 +535,10 @@ class _Gen:
                 n = b.shape[1]
                 prev = seen.get(id(r))
                 seen[id(r)] = n if prev in (None, n) else False
+                widths[id(r)] = r.dtype.width
             for rid, n in seen.items():
-                if n is False:
-                    continue
-                width = next(o.ins[1].root().dtype.width for o in rp.ops
-                             if o.kind == "matmul" and id(o.ins[1].root()) == rid)
-                if width not in (4, 8):
+                width = widths[rid]
+                if n is False or width not in (4, 8):
                     continue
                 vw = 16 // width
                 # N dividing the vector: rows pack densely (one load spans rows)
@@ -310,9 +547,16 @@ class _Gen:
     # -- operand access -------------------------------------------------------------
     def _input(self, x: LV) -> None:
         r = x.root()
-        if id(r) in self.ptr_of or id(r) in self.produced:
+        if id(r) in self.produced or (r.kind == "const" and r.imm is not None):
             return
-        if r.kind == "const" and r.imm is not None:
+        if id(r) in self.ptr_of:
+            k = self.ptr_of[id(r)]
+            if (self.P.layout_of(x)[0] == UNI and not self.rp.uniform_only
+                    and id(r) not in self.uni_names):
+                # slot taken by a loop's stacked operand; stage it on its own too
+                pidx, _ = self._stage(r, f"s{k}", [k])
+                self.uni_names[id(r)] = [f"sf::lds(&s{k}[{p}])" for p in pidx]
+                self.smem_name[id(r)] = (f"s{k}", "")
             return
         k = len(self.ext)
         self.ptr_of[id(r)] = k
@@ -329,28 +573,59 @@ class _Gen:
                 f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{idx} + {j}];" if w > 1 else
                 f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[r];" for j, nm in enumerate(names)))
         elif self.rp.uniform_only:
-            # uniform kernel: loops read straight from global memory (uni_ref)
-            self.ext_kind.append(UNI)
-        else:
+            # uniform kernel: every global operand is put in flight at kernel
+            # start (cp.async into shared memory), so the op loops that follow
+            # never wait on a global load one after the other
             self.ext_kind.append(UNI)
             n = r.numel
             width = r.dtype.width
+            if width in (4, 8) and self.uni_smem + n * width <= UNIFORM_SMEM_BYTES:
+                self.uni_smem += n * width
+                self.staged[id(r)] = f"g{k}"
+                self.smem.append(
+                    f"  __shared__ __align__(16) {ct} g{k}[{max(1, n)}];\n"
+                    f"  for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
+                    f"sf::cp_async<{width}>(&g{k}[q], &((const {ct}*)a.p[{k}])[q]);")
+        else:
+            self.ext_kind.append(UNI)
+            pidx, _ = self._stage(r, f"s{k}", [k])
+            self.uni_names[id(r)] = [f"sf::lds(&s{k}[{p}])" for p in pidx]
+            self.smem_name[id(r)] = (f"s{k}", "")
+
+    def _stage(self, r: LV, name: str, slots: List[int]):
+        """Stage uniform operand(s) of r's shape into shared array ``name``
+        (one slice per pointer slot, padded rows for matvec weights).
+        Returns (padded index of each flat element, slice size)."""
+        ct = _CTYPE[r.dtype]
+        n = r.numel
+        width = r.dtype.width
+        if id(r) in self.pad:
+            N, Np = self.pad[id(r)]
+            off = f"(q / {N}) * {Np} + q % {N}"
+            pidx = [(q // N) * Np + q % N for q in range(n)]
+            size = (n // N) * Np
+        else:
+            off, pidx, size = "q", list(range(n)), n
+        self.smem.append(f"  __shared__ __align__(16) {ct} {name}[{max(1, size * len(slots))}];")
+        head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= 128 else
+                f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) ")
+        for i, k in enumerate(slots):
+            dst = f"{name}[{i * size} + {off}]" if i else f"{name}[{off}]"
             src_q = f"((const {ct}*)a.p[{k}])[q]"
-            if id(r) in self.pad:
-                N, Np = self.pad[id(r)]
-                dst = f"s{k}[(q / {N}) * {Np} + q % {N}]"
-                pidx = [(q // N) * Np + q % N for q in range(n)]
-                size = (n // N) * Np
-            else:
-                dst, pidx, size = f"s{k}[q]", list(range(n)), n
             copy = (f"sf::cp_async<{width}>(&{dst}, &{src_q});" if width in (4, 8)
                     else f"{dst} = {src_q};")
-            head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= 128 else
-                    f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) ")
-            self.smem.append(f"  __shared__ __align__(16) {ct} s{k}[{max(1, size)}];\n"
-                             f"  {head}{copy}")
-            self.uni_names[id(r)] = [f"sf::lds(&s{k}[{p}])" for p in pidx]
-            self.smem_name[id(r)] = f"s{k}"
+            self.smem.append(f"  {head}{copy}")
+        return pidx, size
+
+    def _ext_slot(self, r: LV, kind: str) -> int:
+        """Pointer slot of an external root without staging it."""
+        k = self.ptr_of.get(id(r))
+        if k is None:
+            k = len(self.ext)
+            self.ptr_of[id(r)] = k
+            self.ext.append(r)
+            self.ext_kind.append(kind)
+        return k
 
     def uni_elem(self, x: LV, flat: int) -> str:
         r = x.root()
@@ -365,12 +640,32 @@ class _Gen:
         if r.kind == "const" and r.imm is not None:
             return c_literal(r.imm, r.dtype)
         if id(r) in self.ptr_of and id(r) not in self.produced:
+            if id(r) in self.staged:
+                return f"{self.staged[id(r)]}[{idx}]"
             k = self.ptr_of[id(r)]
             ct = _CTYPE[r.dtype]
             if ct == "bool":
                 return f"((const bool*)a.p[{k}])[{idx}]"
             return f"__ldg((const {ct}*)a.p[{k}] + ({idx}))"
-        return f"U{r.id}[{idx}]"
+        return f"U{self.alias.get(id(r), r).id}[{idx}]"
+
+    def _canon(self, x: LV) -> LV:
+        r = x.root()
+        return self.alias.get(id(r), r)
+
+    def _cse_key(self, op: LOp):
+        if op.kind not in ("ew", "matmul", "transpose", "eye", "reduce"):
+            return None
+        ins = []
+        for x in op.ins:
+            r = x.root()
+            if r.kind == "const" and r.imm is not None:
+                ins.append(("imm", repr(r.imm), r.dtype.value, tuple(x.shape)))
+            else:
+                ins.append((id(self._canon(x)), tuple(x.shape)))
+        o = op.outs[0]
+        return (op.kind, op.name, repr(sorted(op.attrs.items())), tuple(ins),
+                o.dtype.value, tuple(o.shape))
 
     def _emit_uniform_loop(self, op: LOp) -> None:
         """Uniform op in the one-warp uniform kernel: a generated loop over the
@@ -381,7 +676,18 @@ class _Gen:
         o = op.outs[0]
         ct = _CTYPE[o.dtype]
         n = o.numel
-        if any(id(x.root()) in self.dirty for x in op.ins):
+        # common subexpressions: a traced graph repeats chain-independent work
+        # (the same weight transposes / embeddings at every leapfrog step);
+        # within this one kernel launch a repeat aliases the first result
+        key = self._cse_key(op)
+        if key is not None:
+            prev = self.cse.get(key)
+            if prev is not None:
+                self.alias[id(o)] = prev
+                self.uni_names[id(o)] = self.uni_names[id(prev)]
+                return
+            self.cse[key] = o
+        if any(id(self._canon(x)) in self.dirty for x in op.ins):
             self.prologue.append("  __syncwarp();")
             self.dirty.clear()
         self.smem.append(f"  __shared__ __align__(16) {ct} U{o.id}[{max(1, n)}];")
@@ -459,6 +765,9 @@ class _Gen:
     # -- emission ---------------------------------------------------------------------
     def emit(self) -> None:
         for op in self.rp.ops:
+            if op.kind == "loop":
+                self._emit_loop(op)
+                continue
             for x in op.ins:
                 self._input(x)
             L = self.P.layout_of(op.outs[0])
@@ -472,6 +781,55 @@ class _Gen:
             for o in op.outs:
                 if id(o) in self.needed:
                     self.outs.append(o)
+
+    def _emit_loop(self, lp: LoopOp) -> None:
+        """for (it = 0; it < m; ++it) { body } with carried/exported registers."""
+        stacked_ids = {id(r) for _, roots in lp.stacked for r in roots}
+        for x in lp.ins:
+            if id(x) not in stacked_ids:
+                self._input(x)
+        for syn, roots in lp.stacked:
+            name = f"S{syn.id}"
+            slots = [self._ext_slot(r, UNI) for r in roots]
+            pidx, size = self._stage(syn, name, slots)
+            self.uni_names[id(syn)] = [f"sf::lds(&{name}[it * {size} + {p}])" for p in pidx]
+            self.smem_name[id(syn)] = (name, f"it * {size} + ")
+        pre = []
+        for syn, init, _src in lp.carried:
+            _, w, rank = self.P.layout_of(syn)
+            ct = _CTYPE[syn.dtype]
+            names = [f"c{syn.id}_{j}" for j in range(w)]
+            pre.append(" ".join(f"{ct} {nm} = {self.row_elem(init, j, w, rank)};"
+                                for j, nm in enumerate(names)))
+            self.rowed_names[id(syn)] = names
+        exp_names = []
+        for e, _b in lp.exports:
+            _, w, _rank = self.P.layout_of(e)
+            ct = _CTYPE[e.dtype]
+            names = [f"e{e.id}_{j}" for j in range(w)]
+            pre.append(" ".join(f"{ct} {nm} = ({ct})0;" for nm in names))
+            exp_names.append(names)
+        pre.append(f"#pragma unroll 1\n    for (int it = 0; it < {lp.m}; ++it) {{")
+        self.body.append("    " + "\n    ".join(pre))
+        for op in lp.body:
+            self._emit_rowed(op, self.P.layout_of(op.outs[0]))
+        post = []
+        for (e, b), names in zip(lp.exports, exp_names):
+            src = self.rowed_names[id(b)]
+            post.append(" ".join(f"{nm} = {s};" for nm, s in zip(names, src)))
+        for syn, _init, b in lp.carried:
+            src = self.rowed_names[id(b)]
+            post.append(" ".join(f"{nm} = {s};" for nm, s in zip(self.rowed_names[id(syn)], src)))
+        post.append("}")
+        for (e, _b), names in zip(lp.exports, exp_names):
+            self.rowed_names[id(e)] = names
+            if id(e) in self.needed:
+                ct = _CTYPE[e.dtype]
+                w = len(names)
+                for j, nm in enumerate(names):
+                    idx = "r" if w == 1 else f"r * {w} + {j}"
+                    post.append(f"(({ct}*)a.p[@O{e.id}@])[{idx}] = {nm};")
+        self.body.append("    " + "\n    ".join(post))
 
     def _new_tmp(self) -> str:
         self.tmp += 1
@@ -530,7 +888,7 @@ class _Gen:
                 # n accumulators advance together (same sequential-k FMA chain
                 # per output as the nested form / the eager kernel)
                 N, Np = self.pad[id(br)]
-                sname = self.smem_name[id(br)]
+                sname, sbase = self.smem_name[id(br)]
                 vw = 16 // br.dtype.width
                 vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
                 comp = "xyzw"
@@ -543,7 +901,7 @@ class _Gen:
                         v = f // vw
                         if v not in vecs:
                             t = self._new_tmp()
-                            stmt.append(f"const {vt} {t} = {ld}(&{sname}[{v * vw}]);")
+                            stmt.append(f"const {vt} {t} = {ld}(&{sname}[{sbase}{v * vw}]);")
                             vecs[v] = t
                         stmt.append(f"{names[c]} = {fma}({xs[kk]}, {vecs[v]}.{comp[f % vw]}, "
                                     f"{names[c]});")
