@@ -24,7 +24,7 @@ from .errors import (CallbackError, DeadVariable, InputMismatch, KernelError, Mi
 from .graph import GraphFunction, Node
 from .kernels import KernelEnv, ordinal_of, relabel
 from .lowering import (FusedGroup, LOp, Lowerer, LV, PlanWriter, SLOT_CONST, SLOT_INPUT,
-                       SLOT_OUTPUT, SLOT_TEMP, fuse, generate_group, pack_ew_step)
+                       SLOT_OUTPUT, SLOT_TEMP, cse, fuse, generate_group, pack_ew_step)
 from .runtime import current_context, get_runtime
 from .tensor import Tensor
 
@@ -116,8 +116,9 @@ class Program:
         self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)
         from .rowfuse import plan_rows
 
+        ops = cse(lw.ops) if fuse_enabled else lw.ops
         keep = frozenset(id(v.root()) for v in self.out_vals)
-        units = fuse(plan_rows(lw.ops, keep) if fuse_enabled else lw.ops, fuse_enabled)
+        units = fuse(plan_rows(ops, keep) if fuse_enabled else ops, fuse_enabled)
         self.segments = self._segment(units)
         self.n_launches = sum(s.n_launches for s in self.segments
                               if isinstance(s, _NativeSegment))
@@ -277,7 +278,7 @@ class Program:
         ptrs = in_slots + out_slots
         n_rng = max(1, len(rng_counts))
         scalars = struct.pack("<qQ", rows, 0) + b"\0" * (8 * n_rng)
-        block = 32 if rp.uniform_only else 128  # uniform kernels are one warp
+        block = rp.block  # one chain per thread; uniform kernels: one warp per op of a level
         payload = struct.pack("<QIIII", kernel, grid, block, 0, len(ptrs))
         payload += struct.pack("<%di" % len(ptrs), *ptrs)
         payload += struct.pack("<I", len(scalars)) + scalars

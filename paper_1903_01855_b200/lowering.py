@@ -271,6 +271,41 @@ class FusedGroup:
         self.ext_inputs: List[LV] = []
 
 
+_PURE_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "eye"))
+
+
+def cse(ops: List[LOp]) -> List[LOp]:
+    """Common-subexpression elimination over deterministic ops.
+
+    A traced sampler recomputes the same chain-independent values (weight
+    transposes, time encodings) once per unrolled step; each repeat becomes
+    an alias of the first result, so it is computed, stored and staged once
+    per call.  Results are unchanged bit for bit (same op, same operands)."""
+    table: Dict[tuple, LV] = {}
+    out: List[LOp] = []
+    for op in ops:
+        if op.kind in _PURE_KINDS and len(op.outs) == 1:
+            ins = []
+            for x in op.ins:
+                r = x.root()
+                if r.kind == "const" and r.imm is not None:
+                    ins.append(("imm", repr(r.imm), r.dtype.value, tuple(x.shape)))
+                else:
+                    ins.append((id(r), tuple(x.shape)))
+            o = op.outs[0]
+            key = (op.kind, op.name, repr(sorted(op.attrs.items())), tuple(ins),
+                   o.dtype.value, tuple(o.shape))
+            prev = table.get(key)
+            if prev is not None:
+                o.kind = "alias"
+                o.base = prev
+                o.producer = None
+                continue
+            table[key] = o
+        out.append(op)
+    return out
+
+
 def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
     """Group consecutive elementwise ops sharing one output shape."""
     units: List[Any] = []

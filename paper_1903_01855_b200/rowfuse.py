@@ -51,13 +51,14 @@ REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 
 class RowProgram:
-    __slots__ = ("ops", "batch", "gen", "uniform_only")
+    __slots__ = ("ops", "batch", "gen", "uniform_only", "block")
 
     def __init__(self, batch: int):
         self.ops: List[LOp] = []
         self.batch = batch
         self.gen = None  # cached generate_rowprog result
         self.uniform_only = False  # single-CTA kernel for chain-independent ops
+        self.block = 128  # threads per CTA (set by code generation)
 
 
 class LoopOp:
@@ -216,7 +217,7 @@ def _make_loop(span: List[LOp], p: int, m: int, planner, users, keep) -> Optiona
                     ext[id(r0)] = r0
                     new_ins.append(x0)
                     continue
-                if any(x is not r for x, r in zip(xs, roots)) or \
+                if any(x.shape != r.shape for x, r in zip(xs, roots)) or \
                         any(r.shape != r0.shape or r.dtype != r0.dtype for r in roots):
                     return None
                 key = tuple(id(r) for r in roots)
@@ -501,7 +502,6 @@ class _Gen:
         self.ext_kind: List[str] = []    # "row" | "uni"
         self.ptr_of: Dict[int, int] = {}
         self.prologue: List[str] = []
-        self.dirty: set = set()   # uniform values written since the last __syncthreads
         self.smem: List[str] = []
         self.body: List[str] = []
         self.rowed_names: Dict[int, List[str]] = {}
@@ -520,6 +520,9 @@ class _Gen:
         self.uni_smem = _uniform_smem(rp) if rp.uniform_only else 0
         self.cse: Dict[tuple, LV] = {}
         self.alias: Dict[int, LV] = {}
+        self.level: Dict[int, int] = {}
+        self.uni_ops: List[Tuple[int, int, str]] = []  # (level, work, code)
+        self.block = 128
         if not rp.uniform_only:
             seen: Dict[int, object] = {}
             widths: Dict[int, int] = {}
@@ -668,9 +671,11 @@ class _Gen:
                 o.dtype.value, tuple(o.shape))
 
     def _emit_uniform_loop(self, op: LOp) -> None:
-        """Uniform op in the one-warp uniform kernel: a generated loop over the
-        output elements (lanes take consecutive elements, no divergence), the
-        result in shared memory; __syncwarp only before reading fresh values."""
+        """Uniform op in the uniform kernel: a generated loop over the output
+        elements run by one warp (lanes take consecutive elements), the result
+        in shared memory.  Ops are grouped by dependency level; the ops of one
+        level are spread over the CTA's warps and levels are separated by
+        __syncthreads (see _uniform_prologue)."""
         from .lowering import _index_expr
 
         o = op.outs[0]
@@ -687,15 +692,13 @@ class _Gen:
                 self.uni_names[id(o)] = self.uni_names[id(prev)]
                 return
             self.cse[key] = o
-        if any(id(self._canon(x)) in self.dirty for x in op.ins):
-            self.prologue.append("  __syncwarp();")
-            self.dirty.clear()
+        level = 1 + max((self.level.get(id(self._canon(x)), -1) for x in op.ins), default=-1)
+        self.level[id(o)] = level
         self.smem.append(f"  __shared__ __align__(16) {ct} U{o.id}[{max(1, n)}];")
         self.uni_names[id(o)] = [f"U{o.id}[{q}]" for q in range(n)]
-        self.dirty.add(id(o))
         k = op.kind
         shape = o.shape
-        loop = f"  for (int f = threadIdx.x; f < {n}; f += 32) {{ "
+        loop = f"  for (int f = lane; f < {n}; f += 32) {{ "
         if k == "ew":
             args = [self.uni_ref(x, _index_expr(x.shape, shape, "f") if x.numel != 1 else "0")
                     for x in op.ins]
@@ -746,7 +749,35 @@ class _Gen:
                     f"U{o.id}[f] = acc[0]{scale};")
         else:
             raise KernelError(f"uniform kernel: unsupported op {k}")
-        self.prologue.append(loop + body + " }")
+        work = n * (op.ins[0].shape[-1] if k == "matmul" else 1)
+        if k == "reduce":
+            work = op.ins[0].numel
+        self.uni_ops.append((level, work, loop + body + " }"))
+
+    def _uniform_prologue(self) -> None:
+        """Level-by-level schedule of the uniform ops over up to 32 warps."""
+        if not self.uni_ops:
+            return
+        levels: Dict[int, List[Tuple[int, str]]] = {}
+        for level, work, code in self.uni_ops:
+            levels.setdefault(level, []).append((work, code))
+        warps = max(1, min(32, max(len(v) for v in levels.values())))
+        self.block = 32 * warps
+        out = ["  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;"]
+        for i, level in enumerate(sorted(levels)):
+            load = [0] * warps
+            assign: List[List[str]] = [[] for _ in range(warps)]
+            for work, code in sorted(levels[level], key=lambda wc: -wc[0]):
+                w = load.index(min(load))
+                load[w] += work + 32
+                assign[w].append(code)
+            for w, codes in enumerate(assign):
+                if codes:
+                    cond = "" if warps == 1 else f"if (warp == {w}) "
+                    out.append(f"  {cond}{{\n  " + "\n  ".join(codes) + "\n  }")
+            if i + 1 < len(levels):
+                out.append("  __syncthreads();")
+        self.prologue = out
 
     def row_elem(self, x: LV, j: int, out_w: int, out_rank: int) -> str:
         """Element of operand x for output column j of a rowed op."""
@@ -777,6 +808,8 @@ class _Gen:
                 self._emit_uniform_loop(op)
             else:
                 self._emit_rowed(op, L)
+        if self.rp.uniform_only:
+            self._uniform_prologue()
         for op in self.rp.ops:
             for o in op.outs:
                 if id(o) in self.needed:
@@ -976,10 +1009,12 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
                               f"(({ct}*)a.p[{k0 + t}])[q] = {src_arr}[q];")
     n_ptr = k0 + len(g.outs)
     n_rng = max(1, len(g.rng_ops))
+    rp.block = g.block if rp.uniform_only else 128
+    bounds = (str(rp.block) if rp.uniform_only or MIN_BLOCKS == 0
+              else f"128, {MIN_BLOCKS}")
     src = [f"struct Params {{ void* p[{max(1, n_ptr)}]; long long rows; "
            f"unsigned long long seed; unsigned long long off[{n_rng}]; }};",
-           f"extern \"C\" __global__ void __launch_bounds__("
-           f"{'128' if MIN_BLOCKS == 0 else f'128, {MIN_BLOCKS}'}) KNAME(const "
+           f"extern \"C\" __global__ void __launch_bounds__({bounds}) KNAME(const "
            "__grid_constant__ Params a) {"]
     loads = [x for x in g.smem if "int q" in x]
     decls = [x for x in g.smem if "int q" not in x]
