@@ -15,6 +15,7 @@ copy accounting (:231-261), so copy counters stay identical.
 from __future__ import annotations
 
 import struct
+import weakref
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from . import _native, dtypes
@@ -37,30 +38,45 @@ def _known(shape) -> bool:
 
 
 def _bind_inputs(gf: GraphFunction, values: Sequence) -> None:
+    """Check every value against its placeholder (reference: executor.py
+    _bind_inputs).  Tensors are immutable and a Variable's dtype and shape
+    never change, so an object that passed for a placeholder passes forever:
+    the captured weights a staged sampler feeds every call are checked on the
+    first call only (weak references: nothing is kept alive, and a dead
+    variable is still reported)."""
     from .state import Variable
 
     if len(values) != len(gf.inputs):
         raise InputMismatch(f"{gf.name} takes {len(gf.inputs)} inputs (including captures), "
                             f"got {len(values)}")
-    for ph, v in zip(gf.inputs, values):
-        if ph.is_variable_ref or isinstance(v, Variable):
-            if not isinstance(v, Variable):
-                raise InputMismatch(f"{gf.name}: input {ph.name!r} expects a variable")
-            if v.dtype is not ph.dtype or (_known(ph.shape) and v.shape != ph.shape):
-                raise InputMismatch(
-                    f"{gf.name}: variable bound to {ph.name!r} is {v.dtype.value}{list(v.shape)}, "
-                    f"expected {ph.dtype.value}{list(ph.shape)}")
+    ok = gf.__dict__.setdefault("_bound_ok", [None] * len(gf.inputs))
+    for i, (ph, v) in enumerate(zip(gf.inputs, values)):
+        w = ok[i]
+        if w is not None and w() is v:
             continue
-        if not isinstance(v, Tensor):
-            raise InputMismatch(f"{gf.name}: input {ph.name!r} expects a tensor, got "
-                                f"{type(v).__name__}")
-        if v._symbolic is not None:
-            raise InputMismatch(f"{gf.name}: symbolic tensor passed for {ph.name!r}")
-        if v.dtype is not ph.dtype or len(v.shape) != len(ph.shape) or any(
-                w is not None and h != w for h, w in zip(v.shape, ph.shape)):
+        _bind_one(gf, ph, v, Variable)
+        ok[i] = weakref.ref(v)
+
+
+def _bind_one(gf, ph, v, Variable) -> None:
+    if ph.is_variable_ref or isinstance(v, Variable):
+        if not isinstance(v, Variable):
+            raise InputMismatch(f"{gf.name}: input {ph.name!r} expects a variable")
+        if v.dtype is not ph.dtype or (_known(ph.shape) and v.shape != ph.shape):
             raise InputMismatch(
-                f"{gf.name}: input {ph.name!r} is {v.dtype.value}{list(v.shape)}, expected "
-                f"{ph.dtype.value}{list(ph.shape)}")
+                f"{gf.name}: variable bound to {ph.name!r} is {v.dtype.value}{list(v.shape)}, "
+                f"expected {ph.dtype.value}{list(ph.shape)}")
+        return
+    if not isinstance(v, Tensor):
+        raise InputMismatch(f"{gf.name}: input {ph.name!r} expects a tensor, got "
+                            f"{type(v).__name__}")
+    if v._symbolic is not None:
+        raise InputMismatch(f"{gf.name}: symbolic tensor passed for {ph.name!r}")
+    if v.dtype is not ph.dtype or len(v.shape) != len(ph.shape) or any(
+            w is not None and h != w for h, w in zip(v.shape, ph.shape)):
+        raise InputMismatch(
+            f"{gf.name}: input {ph.name!r} is {v.dtype.value}{list(v.shape)}, expected "
+            f"{ph.dtype.value}{list(ph.shape)}")
 
 
 # ---------------------------------------------------------------------------
@@ -425,7 +441,11 @@ class Program:
     @staticmethod
     def _ptr_of(env, root: LV) -> int:
         h = env[id(root)]
-        if isinstance(h, _native.DeviceBuffer):
+        t = type(h)
+        if t is Tensor:
+            b = h._buf
+            return b.ptr if b is not None else h._ptr()
+        if t is _native.DeviceBuffer:
             return h.ptr
         if isinstance(h, Tensor):
             return h._ptr()

@@ -46,6 +46,8 @@ CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "4800"))
 # MIN_BLOCKS)); 0 = no minimum, ptxas picks (best in the sweep once the
 # weights are read with volatile vector loads: ~96 registers, no spills)
 MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
+# matvec weight vectors loaded ahead of their FMAs (latency hiding vs registers)
+PREFETCH = int(__import__("os").environ.get("SF_PREFETCH", "4"))
 # re-roll repeated blocks of row ops into loops (LoopOp)
 REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
@@ -926,16 +928,34 @@ class _Gen:
                 vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
                 comp = "xyzw"
                 lines.append(" ".join(f"{ct} {nm} = ({ct})0;" for nm in names))
-                vecs: Dict[int, str] = {}   # vector index -> temp (short-lived)
+                # weight vectors in first-use order, issued PREFETCH vectors
+                # ahead of the FMAs that consume them (volatile loads keep
+                # program order, so this is the issue order)
+                order: List[int] = []
+                for kk in range(kk_n):
+                    for c in range(n):
+                        v = (kk * Np + c) // vw
+                        if not order or order[-1] != v:
+                            if v not in order:
+                                order.append(v)
+                vecs: Dict[int, str] = {}
+                issued = 0
+
+                def issue_upto(limit, stmt):
+                    nonlocal issued
+                    while issued < min(limit, len(order)):
+                        v = order[issued]
+                        t = self._new_tmp()
+                        stmt.append(f"const {vt} {t} = {ld}(&{sname}[{sbase}{v * vw}]);")
+                        vecs[v] = t
+                        issued += 1
+
                 for kk in range(kk_n):
                     stmt = []
                     for c in range(n):
                         f = kk * Np + c
                         v = f // vw
-                        if v not in vecs:
-                            t = self._new_tmp()
-                            stmt.append(f"const {vt} {t} = {ld}(&{sname}[{sbase}{v * vw}]);")
-                            vecs[v] = t
+                        issue_upto(order.index(v) + 1 + PREFETCH, stmt)
                         stmt.append(f"{names[c]} = {fma}({xs[kk]}, {vecs[v]}.{comp[f % vw]}, "
                                     f"{names[c]});")
                     lines.append(" ".join(stmt))

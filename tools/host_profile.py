@@ -20,4 +20,4 @@ print(f"host {host*1e6:.1f} us/call, wall {wall*1e6:.1f} us/step")
 pr = cProfile.Profile(); pr.enable()
 for _ in range(n): s.step()
 pr.disable(); _native.sync(0)
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats(sys.argv[2] if len(sys.argv) > 2 else "tottime").print_stats(30)
