@@ -58,16 +58,48 @@ def _peaks():
 
 
 class Clocks:
+    """SM clock + throttle reasons sampled DURING the timed region.
+
+    The timed region of the headline is a few ms, far below nvidia-smi's
+    100 ms loop, so NVML is polled in-process every ~2 ms from a helper
+    thread (ctypes releases the GIL); nvidia-smi is the fallback."""
     QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits
+    NVML_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+                 "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = (pynvml, h, reasons, mx)
+            self.stop = threading.Event()
+
+            def poll():
+                while True:
+                    self._nvml_row()
+                    if self.stop.wait(0.002):
+                        break
+
+            self._nvml_row()
+            self.reader = threading.Thread(target=poll, daemon=True)
+            self.reader.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
@@ -75,21 +107,47 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.reader = threading.Thread(target=self._read, daemon=True)
             self.reader.start()
+            # the timed region can be a few ms: make sure the sampler is live
+            # (first row in) before it starts, and take one more row at exit
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
+
+    def _nvml_row(self):
+        pynvml, h, reasons, mx = self.nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        bits = reasons(h)
+        self.rows.append([str(sm), str(mx)] + ["Active" if bits & b else "Not Active"
+                                               for b in self.NVML_BITS.values()])
 
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.reader.join(timeout=5)
+            self._nvml_row()
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=10).stdout
+                for line in out.splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
 
     def summary(self):
         sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]

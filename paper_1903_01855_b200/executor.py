@@ -130,8 +130,10 @@ class Program:
             lv.index = i
             self.in_vals.append(lv)
         self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)
+        from . import rowfuse
         from .rowfuse import plan_rows
 
+        rowfuse.SM_COUNT = _sm_count(self.dev)
         ops = cse(lw.ops) if fuse_enabled else lw.ops
         keep = frozenset(id(v.root()) for v in self.out_vals)
         units = fuse(plan_rows(ops, keep) if fuse_enabled else ops, fuse_enabled)

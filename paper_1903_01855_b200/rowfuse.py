@@ -46,6 +46,8 @@ CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "4800"))
 # MIN_BLOCKS)); 0 = no minimum, ptxas picks (best in the sweep once the
 # weights are read with volatile vector loads: ~96 registers, no spills)
 MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
+# SMs of the target GPU (B200: 148); set by the executor from the device
+SM_COUNT = 148
 # matvec weight vectors loaded ahead of their FMAs (latency hiding vs registers)
 PREFETCH = int(__import__("os").environ.get("SF_PREFETCH", "4"))
 # re-roll repeated blocks of row ops into loops (LoopOp)
@@ -1030,8 +1032,15 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
     n_ptr = k0 + len(g.outs)
     n_rng = max(1, len(g.rng_ops))
     rp.block = g.block if rp.uniform_only else 128
-    bounds = (str(rp.block) if rp.uniform_only or MIN_BLOCKS == 0
-              else f"128, {MIN_BLOCKS}")
+    mb = MIN_BLOCKS
+    if not rp.uniform_only and mb == 0:
+        # fit the whole batch in ONE wave when a register cap allows it: with
+        # 1e5 chains, 782 CTAs need 6 per SM, i.e. <= 80 registers (an 87-
+        # register kernel ran 5/SM and spilled 42 CTAs into a second wave)
+        per_sm = -(-(-(-rp.batch // 128)) // SM_COUNT)
+        if 2 <= per_sm <= 7:
+            mb = per_sm
+    bounds = str(rp.block) if rp.uniform_only or mb == 0 else f"128, {mb}"
     src = [f"struct Params {{ void* p[{max(1, n_ptr)}]; long long rows; "
            f"unsigned long long seed; unsigned long long off[{n_rng}]; }};",
            f"extern \"C\" __global__ void __launch_bounds__({bounds}) KNAME(const "
