@@ -453,7 +453,36 @@ def extras(sf, np, _native, plugins, l2hmc):
     c2["staged_over_eager"] = c2["staged"]["ops_per_sec"] / c2["eager"]["ops_per_sec"]
     out["c2_microbench"] = c2
     out["c4_resnet50_b32"] = resnet_extra(sf, np, _native)
+    out["f1_device_while"] = while_extra(sf, np, _native)
     return out
+
+
+def while_extra(sf, np, _native):
+    """a staged while_loop (1000 iterations of a small matvec
+    body on (64, 8)) with the predicate read on the host every iteration vs.
+    kept on the device (CUDA graph WHILE node)."""
+    from paper_1903_01855_b200 import executor
+
+    sf.init_runtime(sf.RuntimeOptions())
+    W = sf.constant(np.random.default_rng(0).standard_normal((8, 8)).astype(np.float32) * 0.3)
+
+    def iterate(x, n):
+        def body(i, v):
+            return sf.sub(i, 1), sf.add(sf.matmul(v, W), sf.mul(v, 0.5))
+
+        return sf.while_loop(lambda i, v: sf.greater(i, 0), body, [n, x])[1]
+
+    x = sf.constant(np.random.default_rng(1).standard_normal((64, 8)).astype(np.float32))
+    n = sf.constant(1000, dtype=sf.int32)
+    row = {}
+    for mode, flag in (("host_predicate", False), ("device_graph", True)):
+        executor.DEVICE_WHILE = flag
+        staged = sf.stage(iterate)
+        dt = _time_steps(lambda: staged(x, n), 3, _native)
+        row[mode] = {"ms_per_loop": dt * 1e3, "us_per_iteration": dt * 1e3}
+    executor.DEVICE_WHILE = True
+    row["speedup"] = row["host_predicate"]["ms_per_loop"] / row["device_graph"]["ms_per_loop"]
+    return row
 
 
 def c5_extra(sf, _native, rank, world, dist):

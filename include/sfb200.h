@@ -167,6 +167,25 @@ int sf_plan_profile(void* plan, int enable);
 int sf_plan_step_stats(void* plan, int step, int* kind, double* total_ms, uint64_t* runs);
 int sf_plan_destroy(void* plan);
 
+/* ------------------------------------------------------- device while_loop */
+/* Replaces the host loop of _while_kernel (stageflow/kernels.py:513-538):
+ * a CUDA graph  [cond -> set_cond] -> WHILE { body -> state copies -> cond
+ * -> set_cond }  recorded by stream capture of the cond/body plans, so the
+ * predicate never travels to the host.  Protocol: create; fixed buffers
+ * (loop state, captures) with sf_while_buffer; capture part 0 (prologue:
+ * cond plan + sf_while_set_cond), then part 1 (body plan, copies, cond plan,
+ * sf_while_set_cond); then sf_while_launch per call.  Blocks allocated while
+ * a capture is open belong to the graph until sf_while_destroy. */
+int sf_while_create(int dev, void** w);
+int sf_while_buffer(void* w, size_t bytes, void** p);
+int sf_while_capture_begin(void* w, int part);
+/* enqueue (inside a capture) the kernel that sets the loop handle from a
+ * device boolean */
+int sf_while_set_cond(void* w, const void* pred);
+int sf_while_capture_end(void* w, int part);
+int sf_while_launch(void* w);
+int sf_while_destroy(void* w);
+
 /* ------------------------------------------------------- counters */
 /* number of kernels this library has launched on `dev` since sf_init */
 int sf_launch_count(int dev, uint64_t* count);

@@ -108,6 +108,13 @@ def _declare(lib: ctypes.CDLL) -> None:
                                                ctypes.POINTER(ctypes.c_double),
                                                ctypes.POINTER(ctypes.c_uint64)]),
         "sf_launch_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
+        "sf_while_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
+        "sf_while_buffer": (ctypes.c_int, [_VP, ctypes.c_size_t, _PVP]),
+        "sf_while_capture_begin": (ctypes.c_int, [_VP, ctypes.c_int]),
+        "sf_while_set_cond": (ctypes.c_int, [_VP, _VP]),
+        "sf_while_capture_end": (ctypes.c_int, [_VP, ctypes.c_int]),
+        "sf_while_launch": (ctypes.c_int, [_VP]),
+        "sf_while_destroy": (ctypes.c_int, [_VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -124,7 +131,9 @@ EXPORTED_SYMBOLS = (
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
     "sf_plan_profile", "sf_plan_step_stats", "sf_im2col", "sf_col2im", "sf_maxpool2d",
     "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad", "sf_gemm_tf32x3",
-    "sf_split_tf32", "sf_im2col_split",
+    "sf_split_tf32", "sf_im2col_split", "sf_while_create", "sf_while_buffer",
+    "sf_while_capture_begin", "sf_while_set_cond", "sf_while_capture_end", "sf_while_launch",
+    "sf_while_destroy",
 )
 
 
@@ -519,5 +528,55 @@ class NativePlan:
             self.handle = 0
             try:
                 _lib.sf_plan_destroy(h)
+            except Exception:
+                pass
+
+
+class WhileGraph:
+    """A device-side while loop (csrc/sf_graph.cu): fixed loop-state buffers
+    plus a CUDA graph with a WHILE conditional node."""
+
+    def __init__(self, dev: int):
+        L = require_device()
+        h = ctypes.c_void_p(0)
+        rc = L.sf_while_create(dev, ctypes.byref(h))
+        if rc:
+            raise _err(L, rc, "while create")
+        self.handle = h.value
+        self.dev = dev
+
+    def buffer(self, nbytes: int) -> int:
+        p = ctypes.c_void_p(0)
+        rc = _lib.sf_while_buffer(self.handle, max(1, nbytes), ctypes.byref(p))
+        if rc:
+            raise _err(_lib, rc, "while buffer")
+        return p.value
+
+    def capture_begin(self, part: int) -> None:
+        rc = _lib.sf_while_capture_begin(self.handle, part)
+        if rc:
+            raise _err(_lib, rc, "while capture begin")
+
+    def set_cond(self, pred_ptr: int) -> None:
+        rc = _lib.sf_while_set_cond(self.handle, pred_ptr)
+        if rc:
+            raise _err(_lib, rc, "while set cond")
+
+    def capture_end(self, part: int) -> None:
+        rc = _lib.sf_while_capture_end(self.handle, part)
+        if rc:
+            raise _err(_lib, rc, "while capture end")
+
+    def launch(self) -> None:
+        rc = _lib.sf_while_launch(self.handle)
+        if rc:
+            raise _err(_lib, rc, "while launch")
+
+    def __del__(self):
+        h = self.handle
+        if h:
+            self.handle = 0
+            try:
+                _lib.sf_while_destroy(h)
             except Exception:
                 pass

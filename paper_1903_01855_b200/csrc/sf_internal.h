@@ -76,12 +76,23 @@ class Allocator {
   size_t bytes_in_use() const { return in_use_; }
   size_t bytes_cached() const { return cached_; }
 
+  // CUDA-graph capture: addresses handed out while a stream capture is open
+  // are baked into the graph, so every block allocated during the capture
+  // is logged, reused only within the capture, and at end_capture handed to
+  // the graph (which gives them back with give_back when it is destroyed).
+  void begin_capture();
+  void end_capture(std::vector<std::pair<void*, size_t>>* owned);
+  void give_back(const std::vector<std::pair<void*, size_t>>& owned);
+
  private:
   static size_t round_size(size_t bytes);
   std::mutex mu_;
   std::unordered_map<size_t, std::vector<void*>> free_;
   std::unordered_map<void*, size_t> live_;
   size_t in_use_ = 0, cached_ = 0;
+  bool capturing_ = false;
+  std::vector<std::pair<void*, size_t>> cap_log_;
+  std::unordered_map<size_t, std::vector<void*>> cap_free_;
 };
 
 struct Device {

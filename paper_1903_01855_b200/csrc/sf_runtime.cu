@@ -93,6 +93,16 @@ int Allocator::alloc(int dev, size_t bytes, void** p) {
   const size_t sz = round_size(bytes);
   {
     std::lock_guard<std::mutex> lk(mu_);
+    if (capturing_) {
+      auto ct = cap_free_.find(sz);
+      if (ct != cap_free_.end() && !ct->second.empty()) {
+        *p = ct->second.back();
+        ct->second.pop_back();
+        live_[*p] = sz;
+        in_use_ += sz;
+        return SF_OK;
+      }
+    }
     auto it = free_.find(sz);
     if (it != free_.end() && !it->second.empty()) {
       *p = it->second.back();
@@ -100,6 +110,7 @@ int Allocator::alloc(int dev, size_t bytes, void** p) {
       live_[*p] = sz;
       in_use_ += sz;
       cached_ -= sz;
+      if (capturing_) cap_log_.emplace_back(*p, sz);
       return SF_OK;
     }
   }
@@ -107,6 +118,10 @@ int Allocator::alloc(int dev, size_t bytes, void** p) {
   cudaError_t e = cudaMalloc(&q, sz);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
+    if (capturing_) {
+      set_error("device " + std::to_string(dev) + ": out of memory during graph capture");
+      return SF_ERR_OOM;
+    }
     // Return the cache to the driver and retry once.
     cudaDeviceSynchronize();
     trim();
@@ -121,6 +136,7 @@ int Allocator::alloc(int dev, size_t bytes, void** p) {
   std::lock_guard<std::mutex> lk(mu_);
   live_[q] = sz;
   in_use_ += sz;
+  if (capturing_) cap_log_.emplace_back(q, sz);
   *p = q;
   return SF_OK;
 }
@@ -136,9 +152,46 @@ int Allocator::release(void* p) {
   const size_t sz = it->second;
   live_.erase(it);
   in_use_ -= sz;
+  if (capturing_) {
+    for (const auto& e : cap_log_) {
+      if (e.first == p) {  // captured block: reusable only inside this capture
+        cap_free_[sz].push_back(p);
+        return SF_OK;
+      }
+    }
+  }
   cached_ += sz;
   free_[sz].push_back(p);
   return SF_OK;
+}
+
+void Allocator::begin_capture() {
+  std::lock_guard<std::mutex> lk(mu_);
+  capturing_ = true;
+  cap_log_.clear();
+  cap_free_.clear();
+}
+
+void Allocator::end_capture(std::vector<std::pair<void*, size_t>>* owned) {
+  std::lock_guard<std::mutex> lk(mu_);
+  for (const auto& e : cap_log_) {
+    auto it = live_.find(e.first);
+    if (it == live_.end()) in_use_ += e.second;  // released inside the capture
+    else live_.erase(it);
+    owned->push_back(e);  // counted in use until the graph gives it back
+  }
+  cap_log_.clear();
+  cap_free_.clear();
+  capturing_ = false;
+}
+
+void Allocator::give_back(const std::vector<std::pair<void*, size_t>>& owned) {
+  std::lock_guard<std::mutex> lk(mu_);
+  for (const auto& e : owned) {
+    in_use_ -= e.second;
+    cached_ += e.second;
+    free_[e.second].push_back(e.first);
+  }
 }
 
 int Allocator::trim() {

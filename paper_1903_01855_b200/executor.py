@@ -135,6 +135,7 @@ class Program:
 
         rowfuse.SM_COUNT = _sm_count(self.dev)
         ops = cse(lw.ops) if fuse_enabled else lw.ops
+        self.has_rng = any(op.kind in ("rng", "dropout") for op in ops)
         keep = frozenset(id(v.root()) for v in self.out_vals)
         units = fuse(plan_rows(ops, keep) if fuse_enabled else ops, fuse_enabled)
         self.segments = self._segment(units)
@@ -507,6 +508,147 @@ def _needs_interpretation(gf: GraphFunction, inputs, device, rt) -> bool:
     if any(n.device is not None and n.device != device for n in gf.nodes):
         return True
     return any(isinstance(v, Tensor) and v.device != device for v in inputs)
+
+
+# ---------------------------------------------------------------------------
+# device-side while_loop
+# ---------------------------------------------------------------------------
+
+DEVICE_WHILE = True
+
+
+def _plain_program(prog: "Program") -> bool:
+    """One native segment, no RNG (counters are reserved at enqueue time, so
+    a recorded graph would replay the same draws), tensors only."""
+    if any(isinstance(s, _PySegment) for s in prog.segments) or len(prog.segments) > 1:
+        return False
+    if prog.has_rng:
+        return False
+    return all(lv.kind == "input" for lv in prog.in_vals)
+
+
+class _WhileProgram:
+    """A while_loop whose predicate never leaves the device.
+
+    The cond and body native plans are recorded once, by stream capture, into
+    a CUDA graph with a WHILE conditional node (csrc/sf_graph.cu); each call
+    copies the loop variables and captures into the graph's fixed buffers,
+    launches the graph and copies the final state out.  The kernels are the
+    plans' own, so results are bit-identical to the host loop's."""
+
+    def __init__(self, cprog: "Program", bprog: "Program", n_vars: int, dev: int):
+        self.n_vars = n_vars
+        self.dev = dev
+        self.cprog, self.bprog = cprog, bprog
+        w = self.graph = _native.WhileGraph(dev)
+        self.sizes = [lv.nbytes for lv in cprog.in_vals]
+        self.state = [w.buffer(n) for n in self.sizes[:n_vars]]
+        self.ccaps = [w.buffer(n) for n in self.sizes[n_vars:]]
+        self.bcaps = [w.buffer(lv.nbytes) for lv in bprog.in_vals[n_vars:]]
+        self.specs = [(lv.dtype, lv.shape, lv.nbytes) for lv in bprog.in_vals[:n_vars]]
+        part = 0
+        try:
+            w.capture_begin(0)
+            w.set_cond(self._run(cprog, self.state + self.ccaps)[0])
+            w.capture_end(0)
+            part = 1
+            w.capture_begin(1)
+            new = self._run(bprog, self.state + self.bcaps)
+            # a new value that IS an old state buffer must be read before any
+            # state buffer is overwritten: stage those through scratch
+            staged = []
+            for k, p in enumerate(new):
+                if p in self.state and p != self.state[k]:
+                    tmp = _native.alloc(dev, self.specs[k][2])
+                    _native.copy_d2d(dev, tmp.ptr, p, self.specs[k][2])
+                    staged.append(tmp)
+                    tmp_ptr, tmp.ptr = tmp.ptr, 0  # owned by the graph from now on
+                    new[k] = tmp_ptr
+            for k, p in enumerate(new):
+                if p != self.state[k]:
+                    _native.copy_d2d(dev, self.state[k], p, self.specs[k][2])
+            w.set_cond(self._run(cprog, self.state + self.ccaps)[0])
+            w.capture_end(1)
+            part = -1
+        except BaseException:
+            if part >= 0:
+                try:
+                    w.capture_end(part)
+                except Exception:
+                    pass
+            raise
+
+    @staticmethod
+    def _run(prog: "Program", ptrs: List[int]) -> List[int]:
+        """Enqueue prog's plan on fixed pointers; device pointers of its outputs."""
+        by_input = {id(lv): p for lv, p in zip(prog.in_vals, ptrs)}
+        out_ptr: Dict[int, int] = {}
+        for seg in prog.segments:
+            outs = seg.plan.run([by_input[id(r)] for r in seg.in_roots])
+            for r, p in zip(seg.out_roots, outs):
+                out_ptr[id(r)] = p   # graph-owned (allocated inside the capture)
+        res = []
+        for lv in prog.out_vals:
+            r = lv.root()
+            if id(r) in out_ptr:
+                res.append(out_ptr[id(r)])
+            elif id(r) in by_input:
+                res.append(by_input[id(r)])
+            else:
+                prog.keep.append(r.tensor)
+                res.append(r.tensor._ptr())
+        return res
+
+    def run(self, state, ccaps, bcaps, device) -> List[Tensor]:
+        dev = self.dev
+        for dst, t, n in zip(self.state + self.ccaps + self.bcaps, list(state) + list(ccaps)
+                             + list(bcaps), self.sizes[:self.n_vars] + self.sizes[self.n_vars:]
+                             + [t.nbytes for t in bcaps]):
+            if n:
+                _native.copy_d2d(dev, dst, t._ptr(), n)
+        self.graph.launch()
+        out = []
+        for (dtype, shape, n), src in zip(self.specs, self.state):
+            buf = _native.alloc(dev, n)
+            if n:
+                _native.copy_d2d(dev, buf.ptr, src, n)
+            out.append(Tensor._adopt(dtype, shape, device, buf))
+        return out
+
+
+def device_while(cond_gf: GraphFunction, body_gf: GraphFunction, state, cond_caps, body_caps,
+                 env: KernelEnv) -> Optional[List[Tensor]]:
+    """Run a while_loop on the device, or return None (caller loops on the
+    host with the same kernels).  The first call of a loop signature runs on
+    the host, which also compiles and loads every kernel; the graph is
+    recorded on the second call."""
+    if not DEVICE_WHILE or any(not isinstance(v, Tensor) for v in
+                               list(state) + list(cond_caps) + list(body_caps)):
+        return None
+    device = env.device
+    cache = body_gf.__dict__.setdefault("_device_while", {})
+    key = (id(cond_gf), device, _signature(list(state) + list(cond_caps)),
+           _signature(list(body_caps)))
+    ent = cache.get(key)
+    if ent is None:
+        cache[key] = "host-once"
+        return None
+    if ent == "host-once":
+        libs = tuple(env.libraries)
+        try:
+            cprog = _program_for(cond_gf, list(state) + list(cond_caps), device, libs)
+            bprog = _program_for(body_gf, list(state) + list(body_caps), device, libs)
+        except Exception:
+            cprog = bprog = None
+        ok = (cprog is not None and _plain_program(cprog) and _plain_program(bprog)
+              and len(cprog.out_vals) == 1 and cprog.out_vals[0].dtype is DType.boolean
+              and len(bprog.out_vals) == len(state))
+        ent = cache[key] = (_WhileProgram(cprog, bprog, len(state), ordinal_of(device))
+                            if ok else "host")
+    if ent == "host":
+        return None
+    get_runtime().stats.count_graph_launch()
+    return ent.run(state, cond_caps, body_caps, device)
 
 
 def execute_graph(gf: GraphFunction, inputs: Sequence, env: Optional[KernelEnv] = None,

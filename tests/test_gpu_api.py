@@ -331,6 +331,56 @@ def test_cond_and_while():
     assert int(sum_to(n).item()) == 21 and int(sf.stage(sum_to)(n).item()) == 21
 
 
+def test_device_while_loop_matches_host_loop():
+    """while_loop on the device (CUDA graph WHILE node, executor.device_while):
+    the first call of a signature loops on the host, later calls replay the
+    recorded graph; both must give the host loop's bits, for any trip count."""
+    from paper_1903_01855_b200 import executor
+
+    rng = np.random.default_rng(5)
+    W = sf.constant(rng.standard_normal((8, 8)).astype(np.float32) * 0.3)
+
+    def iterate(x, n):
+        def body(i, v):
+            return sf.sub(i, 1), sf.add(sf.matmul(v, W), sf.mul(v, 0.5))
+
+        _, out = sf.while_loop(lambda i, v: sf.greater(i, 0), body, [n, x])
+        return out
+
+    staged = sf.stage(iterate)
+    x = sf.constant(rng.standard_normal((64, 8)).astype(np.float32))
+    cases = [0, 1, 7, 40, 3]
+    executor.DEVICE_WHILE = False
+    try:
+        want = [staged(x, sf.constant(k, dtype=sf.int32)).numpy() for k in cases]
+    finally:
+        executor.DEVICE_WHILE = True
+    got = [staged(x, sf.constant(k, dtype=sf.int32)).numpy() for k in cases * 2]
+    for g, w in zip(got, want * 2):
+        assert g.tobytes() == w.tobytes()
+    progs = [v for gf in _while_bodies(staged) for v in gf.__dict__.get("_device_while",
+                                                                       {}).values()]
+    assert any(isinstance(p, executor._WhileProgram) for p in progs)
+    # int32 accumulation as in the reference's own test (stageflow tests: 21)
+    def sum_to(n):
+        _, acc = sf.while_loop(lambda i, acc: sf.greater(i, 0),
+                               lambda i, acc: (sf.sub(i, 1), sf.add(acc, i)),
+                               [n, sf.constant(0, dtype=sf.int32)])
+        return acc
+
+    s = sf.stage(sum_to)
+    assert [int(s(sf.constant(k, dtype=sf.int32)).item()) for k in (6, 6, 100, 0)] == \
+        [21, 21, 5050, 0]
+
+
+def _while_bodies(pf):
+    out = []
+    for cf in pf.cached_functions():
+        for gf in cf.graph.library.values():
+            out.append(gf)
+    return out
+
+
 # ---------------------------------------------------------------- graph functions
 def test_constant_fold_and_execute():
     b = GraphBuilder()
