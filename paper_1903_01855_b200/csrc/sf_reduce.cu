@@ -76,10 +76,21 @@ __global__ void reduce_chunks(const RedArgs a, const T* __restrict__ in, A* __re
     if (len > a.chunk) len = a.chunk;
     A acc = A();
     bool present = false;
-    for (long long j = lane; j < len; j += 32) {
-      const A v = (A)in[base + red_offset(a, j0 + j)];
-      acc = present ? cadd(acc, v) : v;
+    if (len == 1024) {
+      // full chunk: issue all 32 loads before folding (same fold order)
+      A v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = (A)in[base + red_offset(a, j0 + lane + 32 * q)];
+      acc = v[0];
+#pragma unroll
+      for (int q = 1; q < 32; ++q) acc = cadd(acc, v[q]);
       present = true;
+    } else {
+      for (long long j = lane; j < len; j += 32) {
+        const A v = (A)in[base + red_offset(a, j0 + j)];
+        acc = present ? cadd(acc, v) : v;
+        present = true;
+      }
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -114,11 +125,25 @@ __global__ void __launch_bounds__(1024) reduce_cols(const T* __restrict__ in, lo
   A acc = A();
   bool present = false;
   if (c < C) {
-#pragma unroll 8
-    for (long long g = tl; g < len; g += 32) {
-      const A v = (A)in[(g0 + g) * C + c];
-      acc = present ? cadd(acc, v) : v;
+    if (len == chunk && chunk == 1024) {
+      // full chunk: this lane's 32 elements are all loaded before the fold,
+      // so the loads overlap (one DRAM latency instead of 32 in a row);
+      // the fold order is unchanged
+      const T* p = in + (g0 + tl) * C + c;
+      A v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = (A)p[(long long)q * 32 * C];
+      acc = v[0];
+#pragma unroll
+      for (int q = 1; q < 32; ++q) acc = cadd(acc, v[q]);
       present = true;
+    } else {
+#pragma unroll 8
+      for (long long g = tl; g < len; g += 32) {
+        const A v = (A)in[(g0 + g) * C + c];
+        acc = present ? cadd(acc, v) : v;
+        present = true;
+      }
     }
   }
   acc_s[tl][tc] = acc;
