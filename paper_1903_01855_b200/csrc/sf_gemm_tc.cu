@@ -197,6 +197,173 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent variant: one CTA per SM walks the output tiles (and split-K
+// slices) round-robin.  Six warps:
+//   warp 0 lane 0: TMA producer over a TC_STAGES ring shared by all tiles
+//   warp 1 lane 0: MMA issuer; the accumulator is DOUBLE-BUFFERED in TMEM
+//                  (2 x BN columns), so the MMAs of tile i+1 run while the
+//                  epilogue drains tile i
+//   warps 2-5    : epilogue; warp w reads TMEM lane quarter (w % 4)
+// mbarriers: full/empty per smem stage; acc_full/acc_empty per TMEM buffer.
+// The MMA sequence per tile is the one of gemm_tc_kernel, so the results are
+// bit-identical to it.
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_persistent(const __grid_constant__ CUtensorMap tAhi,
+                       const __grid_constant__ CUtensorMap tAlo,
+                       const __grid_constant__ CUtensorMap tBhi,
+                       const __grid_constant__ CUtensorMap tBlo, float* __restrict__ C, int M,
+                       int N, int K, int kb_per_split, int tiles_n, int tiles_mn, int n_tiles) {
+  constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4, B_BYTES = BN * TC_BK * 4;
+  constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + TC_STAGES * STAGE_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* acc_full = empty + TC_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const int nk_all = (K + TC_BK - 1) / TC_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t g = 0;  // k-blocks issued so far (all tiles): ring position
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int z = t / tiles_mn, mn = t - z * tiles_mn;
+        const int m0 = (mn / tiles_n) * TC_BM, n0 = (mn % tiles_n) * BN;
+        const int kb0 = z * kb_per_split;
+        const int kb1 = kb0 + kb_per_split < nk_all ? kb0 + kb_per_split : nk_all;
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % TC_STAGES;
+          if (g >= TC_STAGES) mbar_wait(&empty[s], ((g / TC_STAGES) & 1u) ^ 1u);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          const int kx = kb * TC_BK;
+          tma_load_2d(st, &tAhi, &full[s], kx, m0);
+          tma_load_2d(st + A_BYTES, &tAlo, &full[s], kx, m0);
+          tma_load_2d(st + 2 * A_BYTES, &tBhi, &full[s], kx, n0);
+          tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(TC_BM >> 4) << 24);
+      uint32_t g = 0;
+      int i = 0;  // local tile count
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int z = t / tiles_mn;
+        const int kb0 = z * kb_per_split;
+        const int kb1 = kb0 + kb_per_split < nk_all ? kb0 + kb_per_split : nk_all;
+        const int b = i & 1;
+        if (i >= 2) mbar_wait(&acc_empty[b], ((uint32_t)(i >> 1) & 1u) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + (uint32_t)(b * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % TC_STAGES;
+          mbar_wait(&full[s], (g / TC_STAGES) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a_hi = base, a_lo = base + A_BYTES;
+          const uint32_t b_hi = base + 2 * A_BYTES, b_lo = base + 2 * A_BYTES + B_BYTES;
+          const uint32_t pa[3] = {a_hi, a_hi, a_lo};
+          const uint32_t pb[3] = {b_hi, b_lo, b_hi};
+#pragma unroll
+          for (int pass = 0; pass < 3; ++pass) {
+#pragma unroll
+            for (int j = 0; j < TC_BK / 8; ++j) {
+              mma_tf32(acc, sw128_desc(pa[pass] + 32u * j), sw128_desc(pb[pass] + 32u * j), idesc,
+                       ((kb - kb0) | pass | j) != 0);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5: TMEM lane quarter q = warp % 4 -> tile rows [32q, 32q + 32)
+    const int q = warp & 3;
+    int i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int z = t / tiles_mn, mn = t - z * tiles_mn;
+      const int m0 = (mn / tiles_n) * TC_BM, n0 = (mn % tiles_n) * BN;
+      const int b = i & 1;
+      mbar_wait(&acc_full[b], (uint32_t)(i >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = m0 + q * 32 + lane;
+      float* Cz = C + (long long)z * M * N;
+      const bool vec = (N & 3) == 0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+            "%10, %11, %12, %13, %14, %15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+              "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+              "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+          float* out = Cz + (long long)row * N + n0 + c0;
+          if (vec && n0 + c0 + 16 <= N) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              reinterpret_cast<float4*>(out)[v] =
+                  make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                              __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (n0 + c0 + e < N) out[e] = __uint_as_float(r[e]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * BN));
+  }
+}
+
 // split-K epilogue: sum of the partial tiles in split order (deterministic)
 __global__ void splitk_reduce(const float* __restrict__ W, float* __restrict__ C, long long mn,
                               int splits) {
@@ -272,13 +439,13 @@ static int run_tc(Device* d, long long M, long long N, long long K, const float*
   const int smem = TC_STAGES * (2 * TC_BM * TC_BK * 4 + 2 * BN * TC_BK * 4) + 1024 + 256;
   static bool configured[64] = {};
   if (!configured[d->id]) {
-    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN>,
+    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured[d->id] = true;
   }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + TC_BM - 1) / TC_BM));
+  const long long tiles_n = (N + BN - 1) / BN, tiles_m = (M + TC_BM - 1) / TC_BM;
   const long long nk = (K + TC_BK - 1) / TC_BK;
-  const long long tiles = (long long)grid.x * grid.y;
+  const long long tiles = tiles_n * tiles_m;
   long long splits = 1;
   if (tiles < d->sm_count && nk >= 64) {  // long contraction, few tiles
     splits = (2LL * d->sm_count + tiles - 1) / tiles;
@@ -288,18 +455,21 @@ static int run_tc(Device* d, long long M, long long N, long long K, const float*
   }
   const long long per = (nk + splits - 1) / splits;
   splits = (nk + per - 1) / per;
+  const long long n_tiles = tiles * splits;
+  const unsigned grid = (unsigned)(n_tiles < d->sm_count ? n_tiles : d->sm_count);
+  float* out = c;
+  float* work = nullptr;
+  if (splits > 1)
+    SF_TRY(d->alloc.alloc(d->id, sizeof(float) * (size_t)(splits * M * N), (void**)&work));
+  if (work) out = work;
+  gemm_tc_persistent<BN><<<grid, 192, smem, d->stream>>>(ta, tal, tb, tbl, out, (int)M, (int)N,
+                                                         (int)K, (int)per, (int)tiles_n,
+                                                         (int)tiles, (int)n_tiles);
   if (splits == 1) {
-    gemm_tc_kernel<BN><<<grid, 128, smem, d->stream>>>(ta, tal, tb, tbl, c, (int)M, (int)N,
-                                                       (int)K, (int)per);
     count_launch(d->id);
     SF_CHECK_CUDA(cudaGetLastError());
     return SF_OK;
   }
-  float* work = nullptr;
-  SF_TRY(d->alloc.alloc(d->id, sizeof(float) * (size_t)(splits * M * N), (void**)&work));
-  grid.z = (unsigned)splits;
-  gemm_tc_kernel<BN><<<grid, 128, smem, d->stream>>>(ta, tal, tb, tbl, work, (int)M, (int)N,
-                                                     (int)K, (int)per);
   long long blocks = (M * N + 255) / 256;
   if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
   splitk_reduce<<<(unsigned)blocks, 256, 0, d->stream>>>(work, c, M * N, (int)splits);
