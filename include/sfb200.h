@@ -137,8 +137,18 @@ int sf_softmax_xent_grad(int dev, int dtype, int64_t rows, int64_t k, const void
  * hi (TF32-representable) + lo parts; k must be a multiple of 4. */
 int sf_gemm_tf32x3(int dev, int64_t m, int64_t n, int64_t k, const void* a_hi, const void* a_lo,
                    const void* b_hi, const void* b_lo, void** c);
+/* General form: a_mn / b_mn = 1 when the operand is stored MN-major
+ * (A as k x m, B as k x n, the GEMM's m / n index contiguous) — e.g. the
+ * activations of a weight-gradient GEMM — so no transposed copy is needed.
+ * ak / bk: contraction rows each operand actually holds (<= k, zero beyond).
+ * Leading dimensions (k-major: ak/bk; MN-major: m/n) must be multiples of 4. */
+int sf_gemm_tf32x3_ex(int dev, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn, int64_t ak,
+                      int64_t bk, const void* a_hi, const void* a_lo, const void* b_hi,
+                      const void* b_lo, void** c);
 /* hi/lo split of an fp32 (rows x cols) matrix; transpose=1 writes the
- * (cols x ldo) transpose with rows zero-padded to ldo. */
+ * (cols x ldo) transpose with rows zero-padded to ldo.  Without transpose,
+ * hi may be NULL: the tensor cores ignore an fp32 operand's low 13 mantissa
+ * bits, so the unsplit matrix can be passed as the hi operand. */
 int sf_split_tf32(int dev, int64_t rows, int64_t cols, int64_t ldo, int transpose, const void* x,
                   void** hi, void** lo);
 

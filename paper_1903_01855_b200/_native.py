@@ -92,6 +92,9 @@ def _declare(lib: ctypes.CDLL) -> None:
                                                  _VP, _VP, _PVP]),
         "sf_gemm_tf32x3": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _I64, _VP, _VP, _VP, _VP,
                                            _PVP]),
+        "sf_gemm_tf32x3_ex": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _I64, ctypes.c_int,
+                                              ctypes.c_int, _I64, _I64, _VP, _VP, _VP, _VP,
+                                              _PVP]),
         "sf_im2col_split": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _I64, _VP, _PVP, _PVP]),
         "sf_split_tf32": (ctypes.c_int, [ctypes.c_int, _I64, _I64, _I64, ctypes.c_int, _VP, _PVP,
                                           _PVP]),
@@ -131,6 +134,7 @@ EXPORTED_SYMBOLS = (
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
     "sf_plan_profile", "sf_plan_step_stats", "sf_im2col", "sf_col2im", "sf_maxpool2d",
     "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad", "sf_gemm_tf32x3",
+    "sf_gemm_tf32x3_ex",
     "sf_split_tf32", "sf_im2col_split", "sf_while_create", "sf_while_buffer",
     "sf_while_capture_begin", "sf_while_set_cond", "sf_while_capture_end", "sf_while_launch",
     "sf_while_destroy",
@@ -152,18 +156,38 @@ def gemm_tf32x3(dev: int, m: int, n: int, k: int, a_hi: int, a_lo: int, b_hi: in
     return nn_call("sf_gemm_tf32x3", dev, m, n, k, a_hi, a_lo, b_hi, b_lo, out_nbytes=m * n * 4)
 
 
+def gemm_tf32x3_ex(dev: int, m: int, n: int, k: int, a_mn: bool, b_mn: bool, ak: int, bk: int,
+                   a_hi: int, a_lo: int, b_hi: int, b_lo: int) -> "DeviceBuffer":
+    """C[m,n] on tcgen05 with per-operand majorness (see sf_gemm_tf32x3_ex)."""
+    return nn_call("sf_gemm_tf32x3_ex", dev, m, n, k, int(a_mn), int(b_mn), ak, bk, a_hi, a_lo,
+                   b_hi, b_lo, out_nbytes=m * n * 4)
+
+
+class RawRef:
+    """A borrowed device pointer (the caller keeps its owner alive)."""
+
+    __slots__ = ("ptr",)
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+
+
 def split_tf32(dev: int, rows: int, cols: int, src: int, transpose: bool = False,
                ldo: int = 0):
-    """(hi, lo) DeviceBuffers of an fp32 matrix (optionally transposed/padded)."""
+    """(hi, lo) of an fp32 matrix (optionally transposed/padded).  Without
+    transpose the hi operand is the source itself (RawRef): the tensor cores
+    ignore the low 13 mantissa bits, so only lo is materialised."""
     L = require_device()
     ldo = ldo or (rows if transpose else cols)
+    raw_hi = not transpose and ldo == cols
     hi, lo = ctypes.c_void_p(0), ctypes.c_void_p(0)
-    rc = L.sf_split_tf32(dev, rows, cols, ldo, int(transpose), src, ctypes.byref(hi),
-                         ctypes.byref(lo))
+    rc = L.sf_split_tf32(dev, rows, cols, ldo, int(transpose), src,
+                         None if raw_hi else ctypes.byref(hi), ctypes.byref(lo))
     if rc:
         raise _err(L, rc, "sf_split_tf32")
     n = (cols if transpose else rows) * ldo * 4
-    return DeviceBuffer(dev, hi.value, n), DeviceBuffer(dev, lo.value, n)
+    hi_ref = RawRef(src) if raw_hi else DeviceBuffer(dev, hi.value, n)
+    return hi_ref, DeviceBuffer(dev, lo.value, n)
 
 
 def nn_call(name: str, dev: int, *args, out_nbytes: int) -> "DeviceBuffer":

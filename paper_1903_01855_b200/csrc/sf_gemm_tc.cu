@@ -70,6 +70,25 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
+// MN-major operand.  For 32-bit (tf32) MN-major operands the only smem
+// layout UMMA accepts is "128B swizzle with 32B atoms" (descriptor layout
+// type 1, SWIZZLE_128B_BASE32B; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B):
+// the plain 128B swizzle makes the MMA read zeros (measured,
+// tools/dev/mn_mma_test.cu).  A tile is MN-chunks of 32 fp32 (128 B) by the
+// k-block's 32 K rows, each chunk one 32x32 TMA box (4096 B): chunks LBO =
+// 4096 B apart, 4-row K groups SBO = 512 B apart (CuTe canonical
+// Swizzle<2,5,2> o ((8,n),(4,k)):((1,LBO),(4,SBO)) in 16-byte units).  One
+// UMMA_K = 8 rows, so k-step j starts 1024 * j bytes in.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(4096u >> 4) << 16;
+  d |= (uint64_t)(512u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)1u << 61;
+  return d;
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -211,7 +230,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // mbarriers: full/empty per smem stage; acc_full/acc_empty per TMEM buffer.
 // The MMA sequence per tile is the one of gemm_tc_kernel, so the results are
 // bit-identical to it.
-template <int BN>
+// AMN / BMN: operand stored MN-major (the GEMM's M / N index contiguous,
+// e.g. A = cols^T of a weight-gradient GEMM read straight from cols): it is
+// loaded as 32x32 boxes and described with sw128_mn_desc, so no transposed
+// copy is ever made.
+template <int BN, bool AMN, bool BMN>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap tAhi,
                        const __grid_constant__ CUtensorMap tAlo,
@@ -267,16 +290,34 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], STAGE_BYTES);
           const int kx = kb * TC_BK;
-          tma_load_2d(st, &tAhi, &full[s], kx, m0);
-          tma_load_2d(st + A_BYTES, &tAlo, &full[s], kx, m0);
-          tma_load_2d(st + 2 * A_BYTES, &tBhi, &full[s], kx, n0);
-          tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
+          if constexpr (AMN) {
+#pragma unroll
+            for (int j = 0; j < TC_BM / 32; ++j) {
+              tma_load_2d(st + 4096 * j, &tAhi, &full[s], m0 + 32 * j, kx);
+              tma_load_2d(st + A_BYTES + 4096 * j, &tAlo, &full[s], m0 + 32 * j, kx);
+            }
+          } else {
+            tma_load_2d(st, &tAhi, &full[s], kx, m0);
+            tma_load_2d(st + A_BYTES, &tAlo, &full[s], kx, m0);
+          }
+          if constexpr (BMN) {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) {
+              tma_load_2d(st + 2 * A_BYTES + 4096 * j, &tBhi, &full[s], n0 + 32 * j, kx);
+              tma_load_2d(st + 2 * A_BYTES + B_BYTES + 4096 * j, &tBlo, &full[s], n0 + 32 * j,
+                          kx);
+            }
+          } else {
+            tma_load_2d(st + 2 * A_BYTES, &tBhi, &full[s], kx, n0);
+            tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) |
+                             ((BMN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
       uint32_t g = 0;
       int i = 0;  // local tile count
@@ -301,8 +342,11 @@ __global__ void __launch_bounds__(192, 1)
           for (int pass = 0; pass < 3; ++pass) {
 #pragma unroll
             for (int j = 0; j < TC_BK / 8; ++j) {
-              mma_tf32(acc, sw128_desc(pa[pass] + 32u * j), sw128_desc(pb[pass] + 32u * j), idesc,
-                       ((kb - kb0) | pass | j) != 0);
+              const uint64_t da = AMN ? sw128_mn_desc(pa[pass] + 1024u * j)
+                                      : sw128_desc(pa[pass] + 32u * j);
+              const uint64_t db = BMN ? sw128_mn_desc(pb[pass] + 1024u * j)
+                                      : sw128_desc(pb[pass] + 32u * j);
+              mma_tf32(acc, da, db, idesc, ((kb - kb0) | pass | j) != 0);
             }
           }
           mma_commit(&empty[s]);
@@ -383,8 +427,8 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
     const float v = x[i];
     const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    hi[i] = h;
-    lo[i] = v - h;
+    if (hi) hi[i] = h;  // hi may be skipped: tcgen05 kind::tf32 ignores the low
+    lo[i] = v - h;      // 13 mantissa bits, so the raw fp32 operand IS hi
   }
 }
 
@@ -410,8 +454,10 @@ __global__ void split_tf32_transpose_kernel(const float* __restrict__ x, float* 
   }
 }
 
+// mn_major: 32x32 boxes in the 128B-swizzle-with-32B-atoms layout that
+// MN-major tf32 UMMA operands require (see sw128_mn_desc)
 static int encode_map(CUtensorMap* map, const float* ptr, long long rows, long long cols,
-                      int box_rows) {
+                      int box_rows, bool mn_major = false) {
   if (!drv.tensorMapEncodeTiled) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return SF_ERR_CUDA;
@@ -420,26 +466,40 @@ static int encode_map(CUtensorMap* map, const float* ptr, long long rows, long l
   const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
   const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  SF_CHECK_CU(drv.tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims,
-                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                       CU_TENSOR_MAP_SWIZZLE_128B,
-                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  SF_CHECK_CU(drv.tensorMapEncodeTiled(
+      map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE,
+      mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   return SF_OK;
 }
 
-template <int BN>
-static int run_tc(Device* d, long long M, long long N, long long K, const float* ahi,
-                  const float* alo, const float* bhi, const float* blo, float* c) {
+// ak / bk: the contraction extent each operand actually stores (<= K; the
+// TMA boxes zero-fill beyond it).  K-major: the row length (leading
+// dimension); MN-major: the number of rows.
+template <int BN, bool AMN, bool BMN>
+static int run_tc(Device* d, long long M, long long N, long long K, long long ak, long long bk,
+                  const float* ahi, const float* alo, const float* bhi, const float* blo,
+                  float* c) {
   CUtensorMap ta, tal, tb, tbl;
-  SF_TRY(encode_map(&ta, ahi, M, K, TC_BM));
-  SF_TRY(encode_map(&tal, alo, M, K, TC_BM));
-  SF_TRY(encode_map(&tb, bhi, N, K, BN));
-  SF_TRY(encode_map(&tbl, blo, N, K, BN));
+  if (AMN) {
+    SF_TRY(encode_map(&ta, ahi, ak, M, 32, true));
+    SF_TRY(encode_map(&tal, alo, ak, M, 32, true));
+  } else {
+    SF_TRY(encode_map(&ta, ahi, M, ak, TC_BM));
+    SF_TRY(encode_map(&tal, alo, M, ak, TC_BM));
+  }
+  if (BMN) {
+    SF_TRY(encode_map(&tb, bhi, bk, N, 32, true));
+    SF_TRY(encode_map(&tbl, blo, bk, N, 32, true));
+  } else {
+    SF_TRY(encode_map(&tb, bhi, N, bk, BN));
+    SF_TRY(encode_map(&tbl, blo, N, bk, BN));
+  }
   const int smem = TC_STAGES * (2 * TC_BM * TC_BK * 4 + 2 * BN * TC_BK * 4) + 1024 + 256;
   static bool configured[64] = {};
   if (!configured[d->id]) {
-    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN>,
+    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN, AMN, BMN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured[d->id] = true;
   }
@@ -462,9 +522,9 @@ static int run_tc(Device* d, long long M, long long N, long long K, const float*
   if (splits > 1)
     SF_TRY(d->alloc.alloc(d->id, sizeof(float) * (size_t)(splits * M * N), (void**)&work));
   if (work) out = work;
-  gemm_tc_persistent<BN><<<grid, 192, smem, d->stream>>>(ta, tal, tb, tbl, out, (int)M, (int)N,
-                                                         (int)K, (int)per, (int)tiles_n,
-                                                         (int)tiles, (int)n_tiles);
+  gemm_tc_persistent<BN, AMN, BMN><<<grid, 192, smem, d->stream>>>(
+      ta, tal, tb, tbl, out, (int)M, (int)N, (int)K, (int)per, (int)tiles_n, (int)tiles,
+      (int)n_tiles);
   if (splits == 1) {
     count_launch(d->id);
     SF_CHECK_CUDA(cudaGetLastError());
@@ -479,15 +539,33 @@ static int run_tc(Device* d, long long M, long long N, long long K, const float*
   return SF_OK;
 }
 
-int launch_gemm_tc(Device* d, int64_t M, int64_t N, int64_t K, const float* ahi, const float* alo,
-                   const float* bhi, const float* blo, float* c) {
+template <int BN>
+static int run_tc_major(Device* d, long long M, long long N, long long K, bool amn, bool bmn,
+                        long long ak, long long bk, const float* ahi, const float* alo,
+                        const float* bhi, const float* blo, float* c) {
+  if (amn && bmn) return run_tc<BN, true, true>(d, M, N, K, ak, bk, ahi, alo, bhi, blo, c);
+  if (amn) return run_tc<BN, true, false>(d, M, N, K, ak, bk, ahi, alo, bhi, blo, c);
+  if (bmn) return run_tc<BN, false, true>(d, M, N, K, ak, bk, ahi, alo, bhi, blo, c);
+  return run_tc<BN, false, false>(d, M, N, K, ak, bk, ahi, alo, bhi, blo, c);
+}
+
+int launch_gemm_tc_ex(Device* d, int64_t M, int64_t N, int64_t K, bool amn, bool bmn, int64_t ak,
+                      int64_t bk, const float* ahi, const float* alo, const float* bhi,
+                      const float* blo, float* c) {
   if (M == 0 || N == 0) return SF_OK;
-  if (K % 4 != 0) {
-    set_error("gemm_tc: K must be a multiple of 4 (16-byte TMA row stride)");
+  // every TMA row stride must be a multiple of 16 bytes
+  const long long a_ld = amn ? M : ak, b_ld = bmn ? N : bk;
+  if (a_ld % 4 != 0 || b_ld % 4 != 0 || ak > K || bk > K || ak <= 0 || bk <= 0) {
+    set_error("gemm_tc: operand leading dimensions must be multiples of 4 and extents <= k");
     return SF_ERR_INVALID;
   }
-  if (N <= 64) return run_tc<64>(d, M, N, K, ahi, alo, bhi, blo, c);
-  return run_tc<128>(d, M, N, K, ahi, alo, bhi, blo, c);
+  if (N <= 64) return run_tc_major<64>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
+  return run_tc_major<128>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
+}
+
+int launch_gemm_tc(Device* d, int64_t M, int64_t N, int64_t K, const float* ahi, const float* alo,
+                   const float* bhi, const float* blo, float* c) {
+  return launch_gemm_tc_ex(d, M, N, K, false, false, K, K, ahi, alo, bhi, blo, c);
 }
 
 int launch_split_tf32(Device* d, int64_t n, const float* x, float* hi, float* lo) {
@@ -525,12 +603,27 @@ int sf_gemm_tf32x3(int dev, int64_t m, int64_t n, int64_t k, const void* a_hi, c
                         (const float*)b_lo, (float*)*c);
 }
 
+int sf_gemm_tf32x3_ex(int dev, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn, int64_t ak,
+                      int64_t bk, const void* a_hi, const void* a_lo, const void* b_hi,
+                      const void* b_lo, void** c) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  if (*c == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(m * n) * 4, c));
+  return launch_gemm_tc_ex(d, m, n, k, a_mn != 0, b_mn != 0, ak, bk, (const float*)a_hi,
+                           (const float*)a_lo, (const float*)b_hi, (const float*)b_lo,
+                           (float*)*c);
+}
+
 int sf_split_tf32(int dev, int64_t rows, int64_t cols, int64_t ldo, int transpose, const void* x,
                   void** hi, void** lo) {
   Device* d;
   SF_TRY(ensure_device(dev, &d));
   const int64_t n = transpose ? cols * ldo : rows * ldo;
-  if (*hi == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * 4, hi));
+  if (hi == nullptr && transpose) {
+    set_error("sf_split_tf32: the hi part may only be skipped without transpose");
+    return SF_ERR_INVALID;
+  }
+  if (hi && *hi == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * 4, hi));
   if (*lo == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * 4, lo));
   if (transpose)
     return launch_split_tf32_t(d, rows, cols, ldo, (const float*)x, (float*)*hi, (float*)*lo);
@@ -538,7 +631,8 @@ int sf_split_tf32(int dev, int64_t rows, int64_t cols, int64_t ldo, int transpos
     set_error("sf_split_tf32: padding only supported with transpose");
     return SF_ERR_INVALID;
   }
-  return launch_split_tf32(d, rows * cols, (const float*)x, (float*)*hi, (float*)*lo);
+  return launch_split_tf32(d, rows * cols, (const float*)x, hi ? (float*)*hi : nullptr,
+                           (float*)*lo);
 }
 
 }  // extern "C"

@@ -91,11 +91,17 @@ def _conv_kernel(attrs, inputs, env):
     if _use_tc(x.dtype):
         kp = _ceil4(k)
         if _is_pointwise(kh, kw, s, p) and kp == k:
-            a = _native.split_tf32(dev, m, k, x._ptr())
+            a = _native.split_tf32(dev, m, k, x._ptr())  # x itself is the hi operand
         else:
             a = _native.im2col_split(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
-        b = _native.split_tf32(dev, k, co, w._ptr(), transpose=True, ldo=kp)  # W^T, (co, kp)
-        out = _tc(dev, m, co, kp, a, b)
+        if co % 4 == 0:
+            # W (k, co) read MN-major: no transposed copy; rows >= k read as 0
+            b = _native.split_tf32(dev, k, co, w._ptr())
+            out = _native.gemm_tf32x3_ex(dev, m, co, kp, False, True, kp, k, a[0].ptr, a[1].ptr,
+                                         b[0].ptr, b[1].ptr)
+        else:
+            b = _native.split_tf32(dev, k, co, w._ptr(), transpose=True, ldo=kp)  # W^T
+            out = _tc(dev, m, co, kp, a, b)
         del a, b
     elif _is_pointwise(kh, kw, s, p):
         out = _mm(dev, x.dtype, m, co, k, x._ptr(), 0, w._ptr(), 0)
@@ -155,7 +161,19 @@ def _conv_gf_kernel(attrs, inputs, env):
     ho, wo = _out_hw(h, wd, kh, s, p)
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
-    if _use_tc(x.dtype):
+    if _use_tc(x.dtype) and co % 4 == 0 and (c % 4 == 0 or not _is_pointwise(kh, kw, s, p)):
+        # dW = cols^T @ dy with both operands read MN-major straight from
+        # cols (m, kp) and dy (m, co): no transposed copies
+        kp = _ceil4(k)
+        if _is_pointwise(kh, kw, s, p):
+            a = _native.split_tf32(dev, m, c, x._ptr())
+        else:
+            a = _native.im2col_split(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
+        b = _native.split_tf32(dev, m, co, dy._ptr())
+        dw = _native.gemm_tf32x3_ex(dev, kp, co, m, True, True, m, m, a[0].ptr, a[1].ptr,
+                                    b[0].ptr, b[1].ptr)  # (kp, co); rows >= k unused
+        del a, b
+    elif _use_tc(x.dtype):
         mp = _ceil4(m)
         if _is_pointwise(kh, kw, s, p):
             a = _native.split_tf32(dev, m, c, x._ptr(), transpose=True, ldo=mp)  # X^T (k, mp)

@@ -52,3 +52,37 @@ def test_split_transpose_padding():
     np.testing.assert_array_equal(h[:, :37] + l_[:, :37], x.T)
     assert not np.any(h[:, 37:]) and not np.any(l_[:, 37:])
     assert np.all((h.view(np.uint32) & 0x1FFF) == 0)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("m,n,k,ak,bk", [(128, 64, 64, 64, 64), (200, 96, 100, 100, 97),
+                                         (516, 256, 3000, 3000, 3000), (36, 128, 33, 33, 33)])
+def test_gemm_mn_major_operands(a_mn, b_mn, m, n, k, ak, bk):
+    """MN-major operands (A stored k x m, B stored k x n) read straight by TMA,
+    no transposed copies; an operand holding fewer than k contraction rows
+    reads zeros beyond them.  Must equal the K-major GEMM on the same data."""
+    rng = np.random.default_rng(m * 7 + n + k)
+    a = np.zeros((m, k), np.float32)
+    b = np.zeros((n, k), np.float32)
+    a[:, :ak] = rng.standard_normal((m, ak))
+    b[:, :bk] = rng.standard_normal((n, bk))
+    if not a_mn and ak % 4:
+        pytest.skip("K-major leading dimension must be a multiple of 4")
+    if not b_mn and bk % 4:
+        pytest.skip("K-major leading dimension must be a multiple of 4")
+    a_store = np.ascontiguousarray(a[:, :ak].T if a_mn else a[:, :ak])
+    b_store = np.ascontiguousarray(b[:, :bk].T if b_mn else b[:, :bk])
+    ta, tb = sf.constant(a_store), sf.constant(b_store)
+    ah, al = _native.split_tf32(0, *a_store.shape, ta._ptr())
+    bh, bl = _native.split_tf32(0, *b_store.shape, tb._ptr())
+    c = _native.gemm_tf32x3_ex(0, m, n, k, a_mn, b_mn, ak, bk, ah.ptr, al.ptr, bh.ptr, bl.ptr)
+    got = _native.download(c, np.float32, (m, n))
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * np.sqrt(k))
+    if k % 4 == 0 and ak == k and bk == k:
+        # same products, same accumulation order as the K-major path: same bits
+        ta2, tb2 = sf.constant(a), sf.constant(b)
+        ah2, al2 = _native.split_tf32(0, m, k, ta2._ptr())
+        bh2, bl2 = _native.split_tf32(0, n, k, tb2._ptr())
+        ref = _native.gemm_tf32x3(0, m, n, k, ah2.ptr, al2.ptr, bh2.ptr, bl2.ptr)
+        assert _native.download(ref, np.float32, (m, n)).tobytes() == got.tobytes()
