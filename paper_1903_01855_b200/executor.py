@@ -293,7 +293,8 @@ class Program:
         in_slots = [use(r) for r in ext]
         out_slots = [define(o) for o in outs]
         rows = rp.batch
-        grid = 1 if rp.uniform_only else max(1, (rows + 127) // 128)  # one chain per thread
+        per_cta = 128 * rp.replicas  # rp.replicas chains per thread
+        grid = 1 if rp.uniform_only else max(1, (rows + per_cta - 1) // per_cta)
         ptrs = in_slots + out_slots
         n_rng = max(1, len(rng_counts))
         scalars = struct.pack("<qQ", rows, 0) + b"\0" * (8 * n_rng)

@@ -46,6 +46,14 @@ CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "4800"))
 # MIN_BLOCKS)); 0 = no minimum, ptxas picks (best in the sweep once the
 # weights are read with volatile vector loads: ~96 registers, no spills)
 MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
+# chains per thread in row kernels: 0 = automatic.  Measured on B200 (L2HMC,
+# 1e5 chains): 2 chains/thread halves the shared-memory weight loads per
+# chain but needs ~160 registers, so the SM holds half the threads; the
+# chains in flight per SM stay the same and the step time did not move
+# (0.207 vs 0.204 ms).  Automatic therefore keeps 1 (REPLICA_MIN_BATCH is
+# the batch from which 2 would be chosen).
+ROW_REPLICAS = int(__import__("os").environ.get("SF_ROW_REPLICAS", "0"))
+REPLICA_MIN_BATCH = 1 << 62
 # SMs of the target GPU (B200: 148); set by the executor from the device
 SM_COUNT = 148
 # matvec weight vectors loaded ahead of their FMAs (latency hiding vs registers)
@@ -55,7 +63,7 @@ REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 
 class RowProgram:
-    __slots__ = ("ops", "batch", "gen", "uniform_only", "block")
+    __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas")
 
     def __init__(self, batch: int):
         self.ops: List[LOp] = []
@@ -63,6 +71,8 @@ class RowProgram:
         self.gen = None  # cached generate_rowprog result
         self.uniform_only = False  # single-CTA kernel for chain-independent ops
         self.block = 128  # threads per CTA (set by code generation)
+        # chains per thread: large batches take 2 (shared weight loads, 2x ILP)
+        self.replicas = ROW_REPLICAS if ROW_REPLICAS else (2 if batch >= REPLICA_MIN_BATCH else 1)
 
 
 class LoopOp:
@@ -527,6 +537,12 @@ class _Gen:
         self.level: Dict[int, int] = {}
         self.uni_ops: List[Tuple[int, int, str]] = []  # (level, work, code)
         self.block = 128
+        # chains per thread: replica k owns row r + 128 k of the CTA's 128 R
+        # rows; the replicas' statements are emitted interleaved, op by op,
+        # so they share every weight load and double the ILP
+        self.R = 1 if rp.uniform_only else rp.replicas
+        self.rep = 0
+        self.rowv = ["r"] + [f"rq{k}" for k in range(1, self.R)]
         if not rp.uniform_only:
             seen: Dict[int, object] = {}
             widths: Dict[int, int] = {}
@@ -551,6 +567,20 @@ class _Gen:
                 # N dividing the vector: rows pack densely (one load spans rows)
                 self.pad[rid] = (n, n if vw % n == 0 else -(-n // vw) * vw)
 
+    @staticmethod
+    def sfx(rep: int) -> str:
+        return "" if rep == 0 else f"q{rep}"
+
+    def _store(self, lines: List[str], o: LV, names_per_rep: List[List[str]]) -> None:
+        """Stores of a needed rowed value (replica k > 0 only if its row exists)."""
+        ct = _CTYPE[o.dtype]
+        for rep, names in enumerate(names_per_rep):
+            w = len(names)
+            rv = self.rowv[rep]
+            st = " ".join(f"(({ct}*)a.p[@O{o.id}@])[{rv if w == 1 else f'{rv} * {w} + {j}'}]"
+                          f" = {nm};" for j, nm in enumerate(names))
+            lines.append(st if rep == 0 else f"if (v{rv}) {{ {st} }}")
+
     # -- operand access -------------------------------------------------------------
     def _input(self, x: LV) -> None:
         r = x.root()
@@ -573,12 +603,16 @@ class _Gen:
         if L[0] == ROW:
             w = L[1]
             self.ext_kind.append(ROW)
-            names = [f"i{k}_{j}" for j in range(w)]
-            self.rowed_names[id(r)] = names
-            idx = "r" if w == 1 else f"r * {w}"
-            self.body.append("    " + " ".join(
-                f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{idx} + {j}];" if w > 1 else
-                f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[r];" for j, nm in enumerate(names)))
+            per_rep = []
+            for rep in range(self.R):
+                names = [f"i{k}_{j}{self.sfx(rep)}" for j in range(w)]
+                per_rep.append(names)
+                rv = self.rowv[rep]
+                self.body.append("    " + " ".join(
+                    f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{rv} * {w} + {j}];" if w > 1 else
+                    f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{rv}];"
+                    for j, nm in enumerate(names)))
+            self.rowed_names[id(r)] = per_rep
         elif self.rp.uniform_only:
             # uniform kernel: every global operand is put in flight at kernel
             # start (cp.async into shared memory), so the op loops that follow
@@ -790,7 +824,7 @@ class _Gen:
             return c_literal(r.imm, r.dtype)
         L = self.P.layout_of(x)
         if L[0] == ROW:
-            names = self.rowed_names[id(r)]
+            names = self.rowed_names[id(r)][self.rep]
             return names[0] if L[1] == 1 else names[j]
         n = x.numel
         if n == 1:
@@ -835,37 +869,38 @@ class _Gen:
         for syn, init, _src in lp.carried:
             _, w, rank = self.P.layout_of(syn)
             ct = _CTYPE[syn.dtype]
-            names = [f"c{syn.id}_{j}" for j in range(w)]
-            pre.append(" ".join(f"{ct} {nm} = {self.row_elem(init, j, w, rank)};"
-                                for j, nm in enumerate(names)))
-            self.rowed_names[id(syn)] = names
+            per_rep = []
+            for rep in range(self.R):
+                self.rep = rep
+                names = [f"c{syn.id}_{j}{self.sfx(rep)}" for j in range(w)]
+                pre.append(" ".join(f"{ct} {nm} = {self.row_elem(init, j, w, rank)};"
+                                    for j, nm in enumerate(names)))
+                per_rep.append(names)
+            self.rep = 0
+            self.rowed_names[id(syn)] = per_rep
         exp_names = []
         for e, _b in lp.exports:
             _, w, _rank = self.P.layout_of(e)
             ct = _CTYPE[e.dtype]
-            names = [f"e{e.id}_{j}" for j in range(w)]
-            pre.append(" ".join(f"{ct} {nm} = ({ct})0;" for nm in names))
-            exp_names.append(names)
+            per_rep = [[f"e{e.id}_{j}{self.sfx(rep)}" for j in range(w)] for rep in range(self.R)]
+            pre.append(" ".join(f"{ct} {nm} = ({ct})0;" for names in per_rep for nm in names))
+            exp_names.append(per_rep)
         pre.append(f"#pragma unroll 1\n    for (int it = 0; it < {lp.m}; ++it) {{")
         self.body.append("    " + "\n    ".join(pre))
         for op in lp.body:
             self._emit_rowed(op, self.P.layout_of(op.outs[0]))
         post = []
-        for (e, b), names in zip(lp.exports, exp_names):
-            src = self.rowed_names[id(b)]
-            post.append(" ".join(f"{nm} = {s};" for nm, s in zip(names, src)))
+        for (e, b), per_rep in zip(lp.exports, exp_names):
+            for names, src in zip(per_rep, self.rowed_names[id(b)]):
+                post.append(" ".join(f"{nm} = {s};" for nm, s in zip(names, src)))
         for syn, _init, b in lp.carried:
-            src = self.rowed_names[id(b)]
-            post.append(" ".join(f"{nm} = {s};" for nm, s in zip(self.rowed_names[id(syn)], src)))
+            for names, src in zip(self.rowed_names[id(syn)], self.rowed_names[id(b)]):
+                post.append(" ".join(f"{nm} = {s};" for nm, s in zip(names, src)))
         post.append("}")
-        for (e, _b), names in zip(lp.exports, exp_names):
-            self.rowed_names[id(e)] = names
+        for (e, _b), per_rep in zip(lp.exports, exp_names):
+            self.rowed_names[id(e)] = per_rep
             if id(e) in self.needed:
-                ct = _CTYPE[e.dtype]
-                w = len(names)
-                for j, nm in enumerate(names):
-                    idx = "r" if w == 1 else f"r * {w} + {j}"
-                    post.append(f"(({ct}*)a.p[@O{e.id}@])[{idx}] = {nm};")
+                self._store(post, e, per_rep)
         self.body.append("    " + "\n    ".join(post))
 
     def _new_tmp(self) -> str:
@@ -901,20 +936,25 @@ class _Gen:
         o = op.outs[0]
         ct = _CTYPE[o.dtype]
         base = f"r{o.id}"
-        names = [f"{base}_{j}" for j in range(w)]
-        self.rowed_names[id(o)] = names
+        per_rep = [[f"{base}_{j}{self.sfx(rep)}" for j in range(w)] for rep in range(self.R)]
+        self.rowed_names[id(o)] = per_rep
         lines = []
         k = op.kind
         if k == "ew":
             for j in range(w):
-                args = [self.row_elem(x, j, w, rank) for x in op.ins]
-                lines.append(f"const {ct} {names[j]} = {ew_expr(op.name, args, ct)};")
+                for rep in range(self.R):
+                    self.rep = rep
+                    args = [self.row_elem(x, j, w, rank) for x in op.ins]
+                    lines.append(f"const {ct} {per_rep[rep][j]} = {ew_expr(op.name, args, ct)};")
         elif k == "matmul":
             a, b = op.ins
             kk_n = a.shape[1]
             n = b.shape[1]
             fma = "__fmaf_rn" if o.dtype is DType.float32 else "__fma_rn"
-            xs = [self.row_elem(a, kk, kk_n, 2) for kk in range(kk_n)]
+            xs_rep = []
+            for rep in range(self.R):
+                self.rep = rep
+                xs_rep.append([self.row_elem(a, kk, kk_n, 2) for kk in range(kk_n)])
             # compiler-only memory fence: keeps NVVM from merging this matvec's
             # weight loads with other uses of the same weights (which would pin
             # hundreds of weights in registers for the whole chunk)
@@ -929,7 +969,8 @@ class _Gen:
                 vw = 16 // br.dtype.width
                 vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
                 comp = "xyzw"
-                lines.append(" ".join(f"{ct} {nm} = ({ct})0;" for nm in names))
+                lines.append(" ".join(f"{ct} {nm} = ({ct})0;" for names in per_rep
+                                      for nm in names))
                 # weight vectors in first-use order, issued PREFETCH vectors
                 # ahead of the FMAs that consume them (volatile loads keep
                 # program order, so this is the issue order)
@@ -958,42 +999,49 @@ class _Gen:
                         f = kk * Np + c
                         v = f // vw
                         issue_upto(order.index(v) + 1 + PREFETCH, stmt)
-                        stmt.append(f"{names[c]} = {fma}({xs[kk]}, {vecs[v]}.{comp[f % vw]}, "
-                                    f"{names[c]});")
+                        for rep in range(self.R):
+                            nm = per_rep[rep][c]
+                            stmt.append(f"{nm} = {fma}({xs_rep[rep][kk]}, "
+                                        f"{vecs[v]}.{comp[f % vw]}, {nm});")
                     lines.append(" ".join(stmt))
             else:
                 for j in range(n):
-                    acc = f"({ct})0"
-                    for kk in range(kk_n):
-                        acc = f"{fma}({xs[kk]}, {self.uni_elem(b, kk * n + j)}, {acc})"
-                    lines.append(f"const {ct} {names[j]} = {acc};")
+                    for rep in range(self.R):
+                        acc = f"({ct})0"
+                        for kk in range(kk_n):
+                            acc = f"{fma}({xs_rep[rep][kk]}, {self.uni_elem(b, kk * n + j)}, {acc})"
+                        lines.append(f"const {ct} {per_rep[rep][j]} = {acc};")
         elif k == "reduce":
             x = op.ins[0]
             xw = self.P.layout_of(x)[1]
-            elems = [self.row_elem(x, j, xw, 2) for j in range(xw)]
-            red = self._cro(elems, ct, lines)
-            if op.name == "reduce_mean":
-                lines.append(f"const {ct} {names[0]} = {red} / ({ct}){float(xw)!r};")
-            else:
-                lines.append(f"const {ct} {names[0]} = {red};")
+            for rep in range(self.R):
+                self.rep = rep
+                elems = [self.row_elem(x, j, xw, 2) for j in range(xw)]
+                red = self._cro(elems, ct, lines)
+                nm = per_rep[rep][0]
+                if op.name == "reduce_mean":
+                    lines.append(f"const {ct} {nm} = {red} / ({ct}){float(xw)!r};")
+                else:
+                    lines.append(f"const {ct} {nm} = {red};")
         elif k == "rng":
             self.rng_ops.append((op, o.numel))
             slot = len(self.rng_ops) - 1
-            for j in range(w):
-                ctr = f"(a.off[{slot}] + (unsigned long long)r * {w}ull + {j}ull)"
-                if op.attrs["kind"] == 0:
-                    val = f"({ct})sf::normal_f64({ctr}, a.seed)"
-                else:
-                    val = (f"sf::uniform_f32({ctr}, a.seed)" if o.dtype is DType.float32
-                           else f"sf::uniform_f64({ctr}, a.seed)")
-                lines.append(f"const {ct} {names[j]} = {val};")
+            for rep in range(self.R):
+                rv = self.rowv[rep]
+                for j in range(w):
+                    ctr = f"(a.off[{slot}] + (unsigned long long){rv} * {w}ull + {j}ull)"
+                    if op.attrs["kind"] == 0:
+                        val = f"({ct})sf::normal_f64({ctr}, a.seed)"
+                    else:
+                        val = (f"sf::uniform_f32({ctr}, a.seed)" if o.dtype is DType.float32
+                               else f"sf::uniform_f64({ctr}, a.seed)")
+                    lines.append(f"const {ct} {per_rep[rep][j]} = {val};")
         else:
             raise KernelError(f"row program: unsupported rowed op {k}")
+        self.rep = 0
         if id(o) in self.needed:
             # store right at the definition so the value's registers free up
-            for j, nm in enumerate(names):
-                idx = "r" if w == 1 else f"r * {w} + {j}"
-                lines.append(f"(({ct}*)a.p[@O{o.id}@])[{idx}] = {nm};")
+            self._store(lines, o, per_rep)
         self.body.append("    " + "\n    ".join(lines))
 
 
@@ -1037,7 +1085,7 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         # fit the whole batch in ONE wave when a register cap allows it: with
         # 1e5 chains, 782 CTAs need 6 per SM, i.e. <= 80 registers (an 87-
         # register kernel ran 5/SM and spilled 42 CTAs into a second wave)
-        per_sm = -(-(-(-rp.batch // 128)) // SM_COUNT)
+        per_sm = -(-(-(-rp.batch // (128 * rp.replicas))) // SM_COUNT)
         if 2 <= per_sm <= 7:
             mb = per_sm
     bounds = str(rp.block) if rp.uniform_only or mb == 0 else f"128, {mb}"
@@ -1061,10 +1109,13 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         name = "sf_uni_" + hashlib.sha1(core.encode()).hexdigest()[:16]
         source = '#include "sf_ops.cuh"\n' + core.replace("KNAME", name)
         return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr
-    # one chain per thread, no loop: nothing is loop-invariant, so nothing
-    # gets hoisted into (and pinned in) registers for the whole kernel
-    src.append("  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;")
+    # R chains per thread (rows r + 128 k of the CTA's 128 R rows; a replica
+    # past the end computes on the last row and does not store)
+    src.append(f"  const long long r = (long long)blockIdx.x * {128 * g.R} + threadIdx.x;")
     src.append("  if (r >= a.rows) return;")
+    for k in range(1, g.R):
+        src.append(f"  const bool vrq{k} = r + {128 * k} < a.rows;")
+        src.append(f"  const long long rq{k} = vrq{k} ? r + {128 * k} : a.rows - 1;")
     src.append("  {")
     src += g.body
     if stores:

@@ -88,3 +88,17 @@ def test_rerolled_program_generates_and_compiles():
             if not u[0].uniform_only:
                 assert "for (int it = 0; it <" in src
             _native.jit_compile(name, src)
+
+
+def test_two_chains_per_thread_codegen(monkeypatch):
+    """Replicated codegen (2 chains per thread) shares the weight loads and
+    guards the second replica's stores."""
+    monkeypatch.setattr(rowfuse, "ROW_REPLICAS", 2)
+    P, keep, out = _steps(6)
+    units = rowfuse.plan_rows(P.ops, keep)
+    for u in units:
+        if isinstance(u, tuple) and not u[0].uniform_only:
+            assert u[0].replicas == 2
+            name, src = rowfuse.generate_rowprog(u[0], u[1], keep)[:2]
+            assert "rq1" in src and "if (vrq1)" in src
+            _native.jit_compile(name, src)
