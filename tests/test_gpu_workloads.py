@@ -90,10 +90,16 @@ def test_l2hmc_staged_row_program():
     assert len(prog.segments) == 1
 
 
-def test_rerolled_loop_bitwise_equals_eager():
+@pytest.mark.parametrize("replicas", [1, 2])
+def test_rerolled_loop_bitwise_equals_eager(replicas, monkeypatch):
     """A traced Python loop with per-step weights and a shared bias: the staged
     row program re-rolls it (carried rows, stacked per-step weights, exported
-    last step) and must match the eager per-op kernels bit for bit."""
+    last step) and must match the eager per-op kernels bit for bit — with one
+    or two chains per thread (1000 rows: the second replica of the last CTA
+    runs past the end and must not store)."""
+    from paper_1903_01855_b200 import rowfuse
+
+    monkeypatch.setattr(rowfuse, "ROW_REPLICAS", replicas)
     plugins.install()
     rng = np.random.default_rng(3)
     B, D, steps = 1000, 6, 7
