@@ -482,6 +482,18 @@ def while_extra(sf, np, _native):
         row[mode] = {"ms_per_loop": dt * 1e3, "us_per_iteration": dt * 1e3}
     executor.DEVICE_WHILE = True
     row["speedup"] = row["host_predicate"]["ms_per_loop"] / row["device_graph"]["ms_per_loop"]
+
+    # cond: the predicate comes out of a device computation each call
+    def branchy(v):
+        flag = sf.greater(sf.reduce_sum(v), 0.0)
+        return sf.cond(flag, lambda u: sf.matmul(u, W), lambda u: sf.mul(u, 0.5), [v])
+
+    for mode, flag in (("cond_host_predicate", False), ("cond_device_graph", True)):
+        executor.DEVICE_COND = flag
+        staged = sf.stage(branchy)
+        dt = _time_steps(lambda: staged(x), 50, _native)
+        row[mode] = {"us_per_call": dt * 1e6}
+    executor.DEVICE_COND = False
     return row
 
 

@@ -187,6 +187,11 @@ int sf_plan_destroy(void* plan);
  * sf_while_set_cond); then sf_while_launch per call.  Blocks allocated while
  * a capture is open belong to the graph until sf_while_destroy. */
 int sf_while_create(int dev, void** w);
+/* Device-side cond (replaces _cond_kernel's host read of the predicate,
+ * stageflow/kernels.py:493-510): same object and protocol, an IF node with
+ * an else branch; parts 0 = prologue (sf_while_set_cond on the predicate
+ * buffer), 1 = then branch, 2 = else branch. */
+int sf_cond_create(int dev, void** w);
 int sf_while_buffer(void* w, size_t bytes, void** p);
 int sf_while_capture_begin(void* w, int part);
 /* enqueue (inside a capture) the kernel that sets the loop handle from a

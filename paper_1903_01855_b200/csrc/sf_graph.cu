@@ -15,6 +15,10 @@
 // bits).  The predicate is consumed on the device by set_cond_kernel, which
 // sets the conditional handle; the host never waits inside the loop.
 //
+// The same object implements cond (stageflow/kernels.py:493-510, which reads
+// the predicate on the host): [set_cond(pred)] -> IF(handle) { then plan ->
+// copy to the output buffers } ELSE { else plan -> copy }.
+//
 // Addresses baked into the graph stay valid because the allocator is in
 // capture mode while the plans are recorded (Allocator::begin_capture): the
 // graph owns every block it was given until sf_while_destroy.
@@ -26,10 +30,15 @@ __global__ void set_cond_kernel(cudaGraphConditionalHandle h, const unsigned cha
   cudaGraphSetConditional(h, pred[0] ? 1u : 0u);
 }
 
+// One graph object serves both control-flow ops:
+//   while (is_if = false): parts 0 = prologue, 1 = loop body
+//   cond  (is_if = true) : parts 0 = prologue (set_cond from the predicate),
+//                          1 = then branch, 2 = else branch (IF node, size 2)
 struct WhileGraph {
   Device* d = nullptr;
+  bool is_if = false;
   cudaGraph_t graph = nullptr;
-  cudaGraph_t body = nullptr;
+  cudaGraph_t body[2] = {nullptr, nullptr};
   cudaGraphExec_t exec = nullptr;
   cudaGraphConditionalHandle handle{};
   std::vector<std::pair<void*, size_t>> owned;  // blocks baked into the graph
@@ -38,14 +47,34 @@ struct WhileGraph {
 };
 
 static int check_part(WhileGraph* w, int part) {
-  if (part != 0 && part != 1) {
-    set_error("sf_while: part must be 0 (prologue) or 1 (body)");
+  const int last = w->is_if ? 2 : 1;
+  if (part < 0 || part > last) {
+    set_error("sf_while: part must be 0 (prologue) or a body index");
     return SF_ERR_INVALID;
   }
-  if (part == 1 && !w->body) {
-    set_error("sf_while: the prologue must be captured before the body");
+  if (part >= 1 && !w->body[0]) {
+    set_error("sf_while: the prologue must be captured before the bodies");
     return SF_ERR_INVALID;
   }
+  return SF_OK;
+}
+
+static int create_graph(int dev, bool is_if, void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  auto* w = new WhileGraph();
+  w->d = d;
+  w->is_if = is_if;
+  cudaError_t e = cudaGraphCreate(&w->graph, 0);
+  if (e == cudaSuccess)
+    e = cudaGraphConditionalHandleCreate(&w->handle, w->graph, 0, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) {
+    if (w->graph) cudaGraphDestroy(w->graph);
+    delete w;
+    set_error(std::string("sf_graph create: ") + cudaGetErrorString(e));
+    return SF_ERR_CUDA;
+  }
+  *out = w;
   return SF_OK;
 }
 
@@ -55,23 +84,9 @@ using namespace sfrt;
 
 extern "C" {
 
-int sf_while_create(int dev, void** out) {
-  Device* d;
-  SF_TRY(ensure_device(dev, &d));
-  auto* w = new WhileGraph();
-  w->d = d;
-  cudaError_t e = cudaGraphCreate(&w->graph, 0);
-  if (e == cudaSuccess)
-    e = cudaGraphConditionalHandleCreate(&w->handle, w->graph, 0, cudaGraphCondAssignDefault);
-  if (e != cudaSuccess) {
-    if (w->graph) cudaGraphDestroy(w->graph);
-    delete w;
-    set_error(std::string("sf_while_create: ") + cudaGetErrorString(e));
-    return SF_ERR_CUDA;
-  }
-  *out = w;
-  return SF_OK;
-}
+int sf_while_create(int dev, void** out) { return create_graph(dev, false, out); }
+
+int sf_cond_create(int dev, void** out) { return create_graph(dev, true, out); }
 
 int sf_while_buffer(void* wp, size_t bytes, void** p) {
   auto* w = (WhileGraph*)wp;
@@ -88,9 +103,9 @@ int sf_while_capture_begin(void* wp, int part) {
     return SF_ERR_INVALID;
   }
   w->d->alloc.begin_capture();
-  cudaError_t e = cudaStreamBeginCaptureToGraph(w->d->stream, part ? w->body : w->graph,
-                                                nullptr, nullptr, 0,
-                                                cudaStreamCaptureModeRelaxed);
+  cudaError_t e = cudaStreamBeginCaptureToGraph(w->d->stream,
+                                                part ? w->body[part - 1] : w->graph, nullptr,
+                                                nullptr, 0, cudaStreamCaptureModeRelaxed);
   if (e != cudaSuccess) {
     w->d->alloc.end_capture(&w->owned);
     set_error(std::string("sf_while_capture_begin: ") + cudaGetErrorString(e));
@@ -139,18 +154,20 @@ int sf_while_capture_end(void* wp, int part) {
     cudaGraphNodeParams params = {};
     params.type = cudaGraphNodeTypeConditional;
     params.conditional.handle = w->handle;
-    params.conditional.type = cudaGraphCondTypeWhile;
-    params.conditional.size = 1;
+    // IF with size 2: body 0 runs when the handle is non-zero, body 1 (else) otherwise
+    params.conditional.type = w->is_if ? cudaGraphCondTypeIf : cudaGraphCondTypeWhile;
+    params.conditional.size = w->is_if ? 2 : 1;
     cudaGraphNode_t node;
     SF_CHECK_CUDA(cudaGraphAddNode(&node, w->graph, leaves.data(), leaves.size(), &params));
-    w->body = params.conditional.phGraph_out[0];
+    w->body[0] = params.conditional.phGraph_out[0];
+    if (w->is_if) w->body[1] = params.conditional.phGraph_out[1];
   }
   return SF_OK;
 }
 
 int sf_while_launch(void* wp) {
   auto* w = (WhileGraph*)wp;
-  if (!w->body || w->capturing >= 0) {
+  if (!w->body[0] || w->capturing >= 0) {
     set_error("sf_while_launch: graph not captured");
     return SF_ERR_INVALID;
   }

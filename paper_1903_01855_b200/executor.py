@@ -516,6 +516,11 @@ def _needs_interpretation(gf: GraphFunction, inputs, device, rt) -> bool:
 # ---------------------------------------------------------------------------
 
 DEVICE_WHILE = True
+# cond as an IF/ELSE graph: correct (tests/test_gpu_api.py) but, measured on
+# B200 (bench extra f1_device_while), 88 us/call against 74 us for the host
+# read — one predicate read is cheaper than the graph launch plus the copies
+# into its fixed buffers — so it is opt-in
+DEVICE_COND = False
 
 
 def _plain_program(prog: "Program") -> bool:
@@ -602,11 +607,16 @@ class _WhileProgram:
 
     def run(self, state, ccaps, bcaps, device) -> List[Tensor]:
         dev = self.dev
-        for dst, t, n in zip(self.state + self.ccaps + self.bcaps, list(state) + list(ccaps)
-                             + list(bcaps), self.sizes[:self.n_vars] + self.sizes[self.n_vars:]
-                             + [t.nbytes for t in bcaps]):
-            if n:
-                _native.copy_d2d(dev, dst, t._ptr(), n)
+        last = self.__dict__.setdefault("last", {})
+        for i, (dst, t) in enumerate(zip(self.state + self.ccaps + self.bcaps,
+                                         list(state) + list(ccaps) + list(bcaps))):
+            if i >= self.n_vars:
+                ref = last.get(i)
+                if ref is not None and ref() is t:
+                    continue  # the same immutable captured tensor: already in place
+                last[i] = weakref.ref(t)
+            if t.nbytes:
+                _native.copy_d2d(dev, dst, t._ptr(), t.nbytes)
         self.graph.launch()
         out = []
         for (dtype, shape, n), src in zip(self.specs, self.state):
@@ -615,6 +625,98 @@ class _WhileProgram:
                 _native.copy_d2d(dev, buf.ptr, src, n)
             out.append(Tensor._adopt(dtype, shape, device, buf))
         return out
+
+
+class _CondProgram:
+    """cond with the predicate read on the device: one CUDA graph
+    [set_cond(pred)] -> IF { then plan -> copy } ELSE { else plan -> copy }
+    (csrc/sf_graph.cu), replacing the host read of _cond_kernel."""
+
+    def __init__(self, tprog: "Program", eprog: "Program", n_ops: int, dev: int):
+        self.dev = dev
+        w = self.graph = _native.WhileGraph(dev, is_if=True)
+        self.pred = w.buffer(1)
+        self.bufs = [w.buffer(lv.nbytes) for lv in tprog.in_vals[:n_ops]]
+        self.bufs += [w.buffer(lv.nbytes) for lv in tprog.in_vals[n_ops:]]
+        self.bufs += [w.buffer(lv.nbytes) for lv in eprog.in_vals[n_ops:]]
+        self.last = [None] * len(self.bufs)  # weakrefs: immutable inputs copied once
+        nt = len(tprog.in_vals)
+        self.specs = [(lv.dtype, lv.shape, lv.nbytes) for lv in tprog.out_vals]
+        self.outs = [w.buffer(n) for _, _, n in self.specs]
+        part = 0
+        try:
+            w.capture_begin(0)
+            w.set_cond(self.pred)
+            w.capture_end(0)
+            for part, (prog, ins) in enumerate(
+                    ((tprog, self.bufs[:nt]), (eprog, self.bufs[:n_ops] + self.bufs[nt:])), 1):
+                w.capture_begin(part)
+                for dst, src, (_, _, n) in zip(self.outs, _WhileProgram._run(prog, ins),
+                                               self.specs):
+                    if n:
+                        _native.copy_d2d(dev, dst, src, n)
+                w.capture_end(part)
+            part = -1
+        except BaseException:
+            if part >= 0:
+                try:
+                    w.capture_end(part)
+                except Exception:
+                    pass
+            raise
+
+    def run(self, pred, values, device) -> List[Tensor]:
+        dev = self.dev
+        _native.copy_d2d(dev, self.pred, pred._ptr(), 1)
+        for i, (dst, t) in enumerate(zip(self.bufs, values)):
+            ref = self.last[i]
+            if ref is not None and ref() is t:
+                continue  # the same immutable tensor as last call: already in place
+            if t.nbytes:
+                _native.copy_d2d(dev, dst, t._ptr(), t.nbytes)
+            self.last[i] = weakref.ref(t)
+        self.graph.launch()
+        out = []
+        for (dtype, shape, n), src in zip(self.specs, self.outs):
+            buf = _native.alloc(dev, n)
+            if n:
+                _native.copy_d2d(dev, buf.ptr, src, n)
+            out.append(Tensor._adopt(dtype, shape, device, buf))
+        return out
+
+
+def device_cond(then_gf: GraphFunction, else_gf: GraphFunction, pred, operands, then_caps,
+                else_caps, env: KernelEnv) -> Optional[List[Tensor]]:
+    """Run a cond with the predicate on the device, or return None (the caller
+    reads it on the host).  Same first-call policy as device_while."""
+    values = list(operands) + list(then_caps) + list(else_caps)
+    if not DEVICE_COND or not isinstance(pred, Tensor) or pred.dtype is not DType.boolean \
+            or pred.size != 1 or any(not isinstance(v, Tensor) for v in values):
+        return None
+    device = env.device
+    cache = then_gf.__dict__.setdefault("_device_cond", {})
+    key = (id(else_gf), device, _signature(list(operands) + list(then_caps)),
+           _signature(list(else_caps)))
+    ent = cache.get(key)
+    if ent is None:
+        cache[key] = "host-once"
+        return None
+    if ent == "host-once":
+        libs = tuple(env.libraries)
+        try:
+            tprog = _program_for(then_gf, list(operands) + list(then_caps), device, libs)
+            eprog = _program_for(else_gf, list(operands) + list(else_caps), device, libs)
+        except Exception:
+            tprog = eprog = None
+        ok = (tprog is not None and _plain_program(tprog) and _plain_program(eprog)
+              and [(v.dtype, v.shape) for v in tprog.out_vals]
+              == [(v.dtype, v.shape) for v in eprog.out_vals])
+        ent = cache[key] = (_CondProgram(tprog, eprog, len(operands), ordinal_of(device))
+                            if ok else "host")
+    if ent == "host":
+        return None
+    get_runtime().stats.count_graph_launch()
+    return ent.run(pred, values, device)
 
 
 def device_while(cond_gf: GraphFunction, body_gf: GraphFunction, state, cond_caps, body_caps,

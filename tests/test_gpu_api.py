@@ -540,3 +540,30 @@ def test_escape_trace():
 
     assert float(f(sf.constant(1.0))) == 6.0 and seen["concrete"]
     assert f.cached_functions()[0].graph.op_counts()["add"] == 1
+
+
+def test_device_cond_matches_host_cond():
+    """cond on the device (CUDA graph IF/ELSE node, executor.device_cond): both
+    branches, repeated calls, captured tensors; bits equal to the host read."""
+    from paper_1903_01855_b200 import executor
+
+    rng = np.random.default_rng(9)
+    W = sf.constant(rng.standard_normal((8, 8)).astype(np.float32))
+
+    def f(x, flag):
+        return sf.cond(flag, lambda v: sf.matmul(v, W), lambda v: sf.mul(sf.neg(v), 2.0), [x])
+
+    staged = sf.stage(f)
+    x = sf.constant(rng.standard_normal((16, 8)).astype(np.float32))
+    flags = [True, False, True, False, False, True]
+    want = [staged(x, sf.constant(b)).numpy() for b in flags]
+    executor.DEVICE_COND = True
+    try:
+        got = [staged(x, sf.constant(b)).numpy() for b in flags * 2]
+    finally:
+        executor.DEVICE_COND = False
+    for g, w in zip(got, want * 2):
+        assert g.tobytes() == w.tobytes()
+    progs = [p for gf in _while_bodies(staged) for p in gf.__dict__.get("_device_cond",
+                                                                      {}).values()]
+    assert any(isinstance(p, executor._CondProgram) for p in progs)
