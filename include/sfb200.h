@@ -192,6 +192,10 @@ int sf_while_create(int dev, void** w);
  * an else branch; parts 0 = prologue (sf_while_set_cond on the predicate
  * buffer), 1 = then branch, 2 = else branch. */
 int sf_cond_create(int dev, void** w);
+/* Whole-program replay: the same object with a single part 0 and no
+ * conditional node — a staged program recorded once by stream capture and
+ * replayed with one graph launch per call (sf_while_launch). */
+int sf_graph_create(int dev, void** w);
 int sf_while_buffer(void* w, size_t bytes, void** p);
 int sf_while_capture_begin(void* w, int part);
 /* enqueue (inside a capture) the kernel that sets the loop handle from a

@@ -113,6 +113,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_launch_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
         "sf_while_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
         "sf_cond_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
+        "sf_graph_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
         "sf_while_buffer": (ctypes.c_int, [_VP, ctypes.c_size_t, _PVP]),
         "sf_while_capture_begin": (ctypes.c_int, [_VP, ctypes.c_int]),
         "sf_while_set_cond": (ctypes.c_int, [_VP, _VP]),
@@ -136,7 +137,8 @@ EXPORTED_SYMBOLS = (
     "sf_plan_profile", "sf_plan_step_stats", "sf_im2col", "sf_col2im", "sf_maxpool2d",
     "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad", "sf_gemm_tf32x3",
     "sf_gemm_tf32x3_ex",
-    "sf_split_tf32", "sf_im2col_split", "sf_while_create", "sf_cond_create", "sf_while_buffer",
+    "sf_split_tf32", "sf_im2col_split", "sf_while_create", "sf_cond_create", "sf_graph_create",
+    "sf_while_buffer",
     "sf_while_capture_begin", "sf_while_set_cond", "sf_while_capture_end", "sf_while_launch",
     "sf_while_destroy",
 )
@@ -562,10 +564,11 @@ class WhileGraph:
     graph with a WHILE conditional node, or (is_if) an IF node with an else
     branch for cond."""
 
-    def __init__(self, dev: int, is_if: bool = False):
+    def __init__(self, dev: int, is_if: bool = False, plain: bool = False):
         L = require_device()
         h = ctypes.c_void_p(0)
-        rc = (L.sf_cond_create if is_if else L.sf_while_create)(dev, ctypes.byref(h))
+        create = L.sf_graph_create if plain else L.sf_cond_create if is_if else L.sf_while_create
+        rc = create(dev, ctypes.byref(h))
         if rc:
             raise _err(L, rc, "while create")
         self.handle = h.value

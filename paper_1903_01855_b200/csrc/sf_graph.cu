@@ -30,13 +30,17 @@ __global__ void set_cond_kernel(cudaGraphConditionalHandle h, const unsigned cha
   cudaGraphSetConditional(h, pred[0] ? 1u : 0u);
 }
 
-// One graph object serves both control-flow ops:
+// One graph object serves both control-flow ops and whole-program replay:
 //   while (is_if = false): parts 0 = prologue, 1 = loop body
 //   cond  (is_if = true) : parts 0 = prologue (set_cond from the predicate),
 //                          1 = then branch, 2 = else branch (IF node, size 2)
+//   plain (plain = true) : part 0 only — a staged program recorded once and
+//                          replayed with one cudaGraphLaunch per call
 struct WhileGraph {
   Device* d = nullptr;
   bool is_if = false;
+  bool plain = false;
+  bool captured = false;
   cudaGraph_t graph = nullptr;
   cudaGraph_t body[2] = {nullptr, nullptr};
   cudaGraphExec_t exec = nullptr;
@@ -47,7 +51,7 @@ struct WhileGraph {
 };
 
 static int check_part(WhileGraph* w, int part) {
-  const int last = w->is_if ? 2 : 1;
+  const int last = w->plain ? 0 : w->is_if ? 2 : 1;
   if (part < 0 || part > last) {
     set_error("sf_while: part must be 0 (prologue) or a body index");
     return SF_ERR_INVALID;
@@ -59,14 +63,17 @@ static int check_part(WhileGraph* w, int part) {
   return SF_OK;
 }
 
-static int create_graph(int dev, bool is_if, void** out) {
+static int create_graph(int dev, bool is_if, bool plain, void** out) {
   Device* d;
   SF_TRY(ensure_device(dev, &d));
   auto* w = new WhileGraph();
   w->d = d;
   w->is_if = is_if;
+  w->plain = plain;
   cudaError_t e = cudaGraphCreate(&w->graph, 0);
-  if (e == cudaSuccess)
+  // (a plain graph must not own a conditional handle: an unused handle makes
+  // cudaGraphInstantiate fail with "invalid argument")
+  if (e == cudaSuccess && !plain)
     e = cudaGraphConditionalHandleCreate(&w->handle, w->graph, 0, cudaGraphCondAssignDefault);
   if (e != cudaSuccess) {
     if (w->graph) cudaGraphDestroy(w->graph);
@@ -84,9 +91,11 @@ using namespace sfrt;
 
 extern "C" {
 
-int sf_while_create(int dev, void** out) { return create_graph(dev, false, out); }
+int sf_while_create(int dev, void** out) { return create_graph(dev, false, false, out); }
 
-int sf_cond_create(int dev, void** out) { return create_graph(dev, true, out); }
+int sf_graph_create(int dev, void** out) { return create_graph(dev, false, true, out); }
+
+int sf_cond_create(int dev, void** out) { return create_graph(dev, true, false, out); }
 
 int sf_while_buffer(void* wp, size_t bytes, void** p) {
   auto* w = (WhileGraph*)wp;
@@ -140,7 +149,8 @@ int sf_while_capture_end(void* wp, int part) {
     set_error(std::string("sf_while_capture_end: ") + cudaGetErrorString(e));
     return SF_ERR_CUDA;
   }
-  if (part == 0) {
+  w->captured = true;
+  if (part == 0 && !w->plain) {
     // append the WHILE node after every leaf of the prologue
     size_t n = 0;
     SF_CHECK_CUDA(cudaGraphGetNodes(w->graph, nullptr, &n));
@@ -167,11 +177,21 @@ int sf_while_capture_end(void* wp, int part) {
 
 int sf_while_launch(void* wp) {
   auto* w = (WhileGraph*)wp;
-  if (!w->body[0] || w->capturing >= 0) {
+  if ((w->plain ? !w->captured : !w->body[0]) || w->capturing >= 0) {
     set_error("sf_while_launch: graph not captured");
     return SF_ERR_INVALID;
   }
-  if (!w->exec) SF_CHECK_CUDA(cudaGraphInstantiate(&w->exec, w->graph, 0));
+  if (!w->exec) {
+    cudaError_t e = cudaGraphInstantiate(&w->exec, w->graph, 0);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      if (const char* dot = getenv("SF_GRAPH_DOT"))  // debugging aid: dump the graph
+        cudaGraphDebugDotPrint(w->graph, dot, cudaGraphDebugDotFlagsVerbose);
+      w->exec = nullptr;
+      set_error(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+      return SF_ERR_CUDA;
+    }
+  }
   SF_CHECK_CUDA(cudaGraphLaunch(w->exec, w->d->stream));
   count_launch(w->d->id);
   return SF_OK;

@@ -427,6 +427,35 @@ class Program:
 
     # -- execution -----------------------------------------------------------------
     def run(self, inputs: Sequence, libraries) -> List[Tensor]:
+        g = self.__dict__.get("_replay")
+        if g is not None and g is not False:
+            outs = g.try_run(inputs)
+            if outs is not None:
+                return outs
+        elif g is None and GRAPH_REPLAY and self._replayable():
+            calls = self.__dict__["_calls"] = self.__dict__.get("_calls", 0) + 1
+            if calls >= 2:  # first call compiled and loaded every kernel
+                try:
+                    self._replay = _ProgramGraph(self, inputs, libraries)
+                except _NotCapturable:
+                    self._replay = False
+                else:
+                    # hand the first replay's outputs over without keeping a
+                    # reference (a kept output would mark the graph busy forever)
+                    outs, self._replay.first_outputs = self._replay.first_outputs, None
+                    return outs
+        return self._run_direct(inputs, libraries)
+
+    def _replayable(self) -> bool:
+        r = self.__dict__.get("_replayable_flag")
+        if r is None:
+            r = (not self.has_rng and self.n_launches >= GRAPH_MIN_LAUNCHES
+                 and all(s.op.name in GRAPH_SAFE_OPS for s in self.segments
+                         if isinstance(s, _PySegment)))
+            self._replayable_flag = r
+        return r
+
+    def _run_direct(self, inputs: Sequence, libraries) -> List[Tensor]:
         env: Dict[int, object] = {}
         for lv, v in zip(self.in_vals, inputs):
             env[id(lv)] = v
@@ -509,6 +538,161 @@ def _needs_interpretation(gf: GraphFunction, inputs, device, rt) -> bool:
     if any(n.device is not None and n.device != device for n in gf.nodes):
         return True
     return any(isinstance(v, Tensor) and v.device != device for v in inputs)
+
+
+# ---------------------------------------------------------------------------
+# whole-program CUDA-graph replay
+# ---------------------------------------------------------------------------
+
+# Programs with at least this many native launches are recorded into a CUDA
+# graph on their second call and replayed with one launch afterwards.
+GRAPH_REPLAY = True
+GRAPH_MIN_LAUNCHES = 16
+# Python-run plugin ops that only enqueue device work on the backend stream
+# (no host reads, no host RNG): safe inside a capture.  nn.install() adds the
+# ResNet ops.
+GRAPH_SAFE_OPS: set = set()
+
+
+class _NotCapturable(Exception):
+    pass
+
+
+class _GraphBuffer(_native.DeviceBuffer):
+    """Device memory owned by a recorded graph: never freed through the
+    allocator; holds the replay's liveness token."""
+
+    __slots__ = ("token",)
+
+    def __init__(self, dev, ptr, nbytes, token):
+        super().__init__(dev, ptr, nbytes)
+        self.token = token
+
+    def __del__(self):
+        pass
+
+
+class _Token:
+    """Liveness of one replay's outputs; keeps the graph (and so the memory
+    the outputs live in) alive while any output is."""
+
+    __slots__ = ("graph", "__weakref__")
+
+    def __init__(self, graph):
+        self.graph = graph
+
+
+class _ProgramGraph:
+    """A staged program recorded once into a CUDA graph (stream capture of its
+    plans and capture-safe Python segments) and replayed with one
+    cudaGraphLaunch per call — "CUDA graphs instead of a tracing compiler".
+
+    Inputs: variables and outputs of other recorded programs are *borrowed*
+    (their addresses are stable; a replay requires the same addresses);
+    every other tensor is copied into a graph-owned buffer each call (skipped
+    when it is the same immutable tensor as last time).  Outputs are the
+    graph's own buffers, handed out zero-copy; while any output of the last
+    replay is alive the graph is busy and the program runs directly instead,
+    so a result is never overwritten under its owner."""
+
+    def __init__(self, prog: "Program", inputs, libraries):
+        from .state import Variable
+
+        self.prog = prog
+        dev = self.dev = prog.dev
+        w = self.graph = _native.WhileGraph(dev, plain=True)
+        self.kinds: List[tuple] = []
+        run_inputs = []
+        for lv, v in zip(prog.in_vals, inputs):
+            if isinstance(v, Variable):
+                self.kinds.append(("borrow", v._storage_ptr()))
+                run_inputs.append(v)
+            elif isinstance(v, Tensor) and isinstance(v._buf, _GraphBuffer):
+                self.kinds.append(("borrow", v._buf.ptr))
+                run_inputs.append(v)
+            elif isinstance(v, Tensor):
+                p = w.buffer(v.nbytes)
+                self.kinds.append(("fixed", p, v.nbytes))
+                run_inputs.append(Tensor._adopt(v.dtype, v.shape, v.device,
+                                                _GraphBuffer(dev, p, v.nbytes, None)))
+            else:
+                raise _NotCapturable("unsupported input")
+        self.last = [None] * len(self.kinds)
+        self._copy_in(inputs)
+        w.capture_begin(0)
+        try:
+            outs = prog._run_direct(run_inputs, libraries)
+        except BaseException:
+            try:
+                w.capture_end(0)
+            except Exception:
+                pass
+            raise
+        w.capture_end(0)
+        inputs_ptrs = {k[1] for k in self.kinds}
+        self.outs = []
+        owned_bufs = []
+        for lv, t in zip(prog.out_vals, outs):
+            buf = t._buf
+            ptr = buf.ptr if buf is not None else 0
+            if lv.root().kind == "const" or buf is None:
+                kind = "static"      # a plan-owned constant: returned as is
+            elif ptr in inputs_ptrs:
+                kind = "copy"        # passes an input through: copied out per call
+            else:
+                kind = "graph"       # allocated inside the capture: graph-owned
+                owned_bufs.append(buf)
+            self.outs.append((kind, t, ptr, t.nbytes))
+        for buf in owned_bufs:
+            buf.ptr = 0              # never freed through the allocator
+        self.token_ref = None
+        self.first_outputs = self._launch()
+
+    def _copy_in(self, inputs) -> None:
+        for i, (k, v) in enumerate(zip(self.kinds, inputs)):
+            if k[0] != "fixed":
+                continue
+            ref = self.last[i]
+            if ref is not None and ref() is v:
+                continue
+            if k[2]:
+                _native.copy_d2d(self.dev, k[1], v._ptr(), k[2])
+            self.last[i] = weakref.ref(v)
+
+    def _launch(self) -> List[Tensor]:
+        self.graph.launch()
+        token = _Token(self.graph)
+        self.token_ref = weakref.ref(token)
+        res = []
+        dev, device = self.dev, self.prog.device
+        for kind, t, ptr, n in self.outs:
+            if kind == "graph":
+                res.append(Tensor._adopt(t.dtype, t.shape, device, _GraphBuffer(dev, ptr, n, token)))
+            elif kind == "copy":
+                buf = _native.alloc(dev, n)
+                if n:
+                    _native.copy_d2d(dev, buf.ptr, ptr, n)
+                res.append(Tensor._adopt(t.dtype, t.shape, device, buf))
+            else:
+                res.append(t)
+        return res
+
+    def try_run(self, inputs) -> Optional[List[Tensor]]:
+        if self.token_ref is not None and self.token_ref() is not None:
+            return None  # outputs of the last replay still alive
+        from .state import Variable
+
+        for k, v in zip(self.kinds, inputs):
+            if k[0] == "borrow":
+                p = v._storage_ptr() if isinstance(v, Variable) else \
+                    (v._buf.ptr if isinstance(v, Tensor) and isinstance(v._buf, _GraphBuffer)
+                     else None)
+                if p != k[1]:
+                    return None
+            elif not isinstance(v, Tensor):
+                return None
+        self._copy_in(inputs)
+        return self._launch()
 
 
 # ---------------------------------------------------------------------------

@@ -287,6 +287,8 @@ def install() -> None:
     from . import plugins
     from .ops import register_op
 
+    from .executor import GRAPH_SAFE_OPS
+
     plugins.install()
     reg = get_runtime().registry
     for d in nn_defs():
@@ -294,6 +296,9 @@ def install() -> None:
             reg.get(d.name)
         except Exception:
             register_op(d)
+        # these kernels only enqueue device work on the backend stream: a staged
+        # program containing them can be recorded into a CUDA graph
+        GRAPH_SAFE_OPS.add(d.name)
 
 
 def conv2d(x, w, stride=1, pad=0):

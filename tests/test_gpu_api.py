@@ -567,3 +567,47 @@ def test_device_cond_matches_host_cond():
     progs = [p for gf in _while_bodies(staged) for p in gf.__dict__.get("_device_cond",
                                                                       {}).values()]
     assert any(isinstance(p, executor._CondProgram) for p in progs)
+
+
+def test_program_graph_replay_semantics():
+    """Whole-program CUDA-graph replay (executor._ProgramGraph): replays give
+    the direct run's bits; fresh input data is copied in; variables are read
+    live; an output still held by the caller is never overwritten (the next
+    call runs directly instead)."""
+    from paper_1903_01855_b200 import executor
+
+    rng = np.random.default_rng(2)
+    Ws = [sf.Variable(sf.constant(rng.standard_normal((64, 64)).astype(np.float32) * 0.2))
+          for _ in range(12)]
+
+    def f(x):
+        h = x
+        for W in Ws:
+            h = sf.relu(sf.matmul(h, W.read_value()))
+        return h, sf.reduce_sum(h)
+
+    def direct(x):
+        executor.GRAPH_REPLAY = False
+        try:
+            return [t.numpy() for t in sf.stage(f)(x)]
+        finally:
+            executor.GRAPH_REPLAY = True
+
+    staged = sf.stage(f)
+    xs = [sf.constant(rng.standard_normal((64, 64)).astype(np.float32)) for _ in range(4)]
+    got = [[t.numpy() for t in staged(x)] for x in xs]           # 2nd call records the graph
+    prog = next(iter(staged.cached_functions()[0].graph._plan.values()))
+    assert isinstance(prog.__dict__.get("_replay"), executor._ProgramGraph)
+    for x, g in zip(xs, got):
+        for a, b in zip(g, direct(x)):
+            assert a.tobytes() == b.tobytes()
+    held = staged(xs[0])                       # keep these outputs alive ...
+    snapshot = [t.numpy().copy() for t in held]
+    other = staged(xs[1])                      # ... so this call must not reuse them
+    assert all(t.numpy().tobytes() == s.tobytes() for t, s in zip(held, snapshot))
+    assert other[0].numpy().tobytes() == direct(xs[1])[0].tobytes()
+    del held, other
+    Ws[3].assign(sf.constant(np.eye(64, dtype=np.float32)))   # variables are read live
+    after = [t.numpy() for t in staged(xs[2])]
+    for a, b in zip(after, direct(xs[2])):
+        assert a.tobytes() == b.tobytes()
