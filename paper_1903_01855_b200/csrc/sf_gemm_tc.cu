@@ -1,22 +1,25 @@
 // sf_gemm_tc.cu — fp32-accurate GEMM on the 5th-generation tensor cores.
 //
-// C[M,N] (fp32, row-major) = A[M,K] . B[N,K]^T with both operands K-major,
-// computed as 3xTF32:  A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi  where
-// hi = x with the low 13 mantissa bits cleared (exactly representable in
-// TF32) and lo = x - hi (exact in fp32).  Relative error ~2^-22, i.e. fp32
-// class — what the ResNet-50 convolutions need to meet the rtol 1e-4
-// contract against the reference's numpy/OpenBLAS arithmetic.
+// C[M,N] (fp32, row-major) = A[M,K] . B[N,K]^T, computed as 3xTF32:
+// A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi  where hi = x with the low 13 mantissa
+// bits cleared (exactly representable in TF32) and lo = x - hi (exact in
+// fp32).  Relative error ~2^-22, i.e. fp32 class — what the ResNet-50
+// convolutions need to meet the rtol 1e-4 contract against the reference's
+// numpy/OpenBLAS arithmetic.  The tensor cores ignore an fp32 operand's low
+// 13 mantissa bits, so the unsplit matrix serves as hi; only lo is stored.
 //
-// Structure (one 128 x BN output tile per CTA, 4 warps):
+// gemm_tc_persistent: one CTA (6 warps) per SM walks the output tiles
 //   warp 0 / lane 0 : TMA producer — 4 tiles (Ahi, Alo, Bhi, Blo) per k-block
-//                     into a 3-stage ring of 128B-swizzled smem, mbarrier
+//                     into a 3-stage ring of swizzled smem, mbarrier
 //                     full/empty handshakes
 //   warp 1 / lane 0 : MMA issuer — tcgen05.mma.cta_group::1.kind::tf32, 3
-//                     passes x 4 k-steps per k-block into one TMEM
-//                     accumulator; tcgen05.commit releases smem slots
-//   warps 0-3       : epilogue — tcgen05.ld 32x32b from their TMEM lane
-//                     quarter, stores to C
-// TMEM: BN fp32 columns allocated by warp 1.
+//                     passes x 4 k-steps per k-block into a double-buffered
+//                     TMEM accumulator; tcgen05.commit releases smem slots
+//   warps 2-5       : epilogue — tcgen05.ld 32x32b from their TMEM lane
+//                     quarter, float4 stores to C, overlapping the next
+//                     tile's MMAs
+// Operands may be K-major (128B swizzle) or MN-major (128B swizzle with 32B
+// atoms, the only MN-major tf32 layout UMMA accepts).
 #include <cudaTypedefs.h>
 
 #include "sf_internal.h"
@@ -104,118 +107,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-template <int BN>
-__global__ void __launch_bounds__(128, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tAhi, const __grid_constant__ CUtensorMap tAlo,
-                   const __grid_constant__ CUtensorMap tBhi, const __grid_constant__ CUtensorMap tBlo,
-                   float* __restrict__ C, int M, int N, int K, int kb_per_split) {
-  constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4, B_BYTES = BN * TC_BK * 4;
-  constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + TC_STAGES * STAGE_BYTES);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tmem_full = empty + TC_STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tmem_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    asm volatile("tcgen05.fence::before_thread_sync;");
-  }
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
-
-  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
-  // split-K: blockIdx.z owns k-blocks [kb0, kb1) and writes its own partial C
-  const int nk_all = (K + TC_BK - 1) / TC_BK;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int kb1 = kb0 + kb_per_split < nk_all ? kb0 + kb_per_split : nk_all;
-  const int nk = kb1 - kb0;
-  C += (long long)blockIdx.z * M * N;
-
-  if (warp == 0 && lane == 0) {
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % TC_STAGES;
-      const uint32_t round = (uint32_t)(kb / TC_STAGES);
-      if (kb >= TC_STAGES) mbar_wait(&empty[s], (round & 1u) ^ 1u);
-      uint8_t* st = smem + s * STAGE_BYTES;
-      mbar_expect_tx(&full[s], STAGE_BYTES);
-      const int kx = (kb0 + kb) * TC_BK;
-      tma_load_2d(st, &tAhi, &full[s], kx, m0);
-      tma_load_2d(st + A_BYTES, &tAlo, &full[s], kx, m0);
-      tma_load_2d(st + 2 * A_BYTES, &tBhi, &full[s], kx, n0);
-      tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = BN
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(TC_BM >> 4) << 24);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % TC_STAGES;
-      mbar_wait(&full[s], (uint32_t)(kb / TC_STAGES) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-      const uint32_t a_hi = base, a_lo = base + A_BYTES;
-      const uint32_t b_hi = base + 2 * A_BYTES, b_lo = base + 2 * A_BYTES + B_BYTES;
-      const uint32_t pa[3] = {a_hi, a_hi, a_lo};
-      const uint32_t pb[3] = {b_hi, b_lo, b_hi};
-#pragma unroll
-      for (int pass = 0; pass < 3; ++pass) {
-#pragma unroll
-        for (int j = 0; j < TC_BK / 8; ++j) {  // UMMA_K = 8 tf32 = 32 bytes
-          mma_tf32(tmem, sw128_desc(pa[pass] + 32u * j), sw128_desc(pb[pass] + 32u * j), idesc,
-                   (kb | pass | j) != 0);
-        }
-      }
-      mma_commit(&empty[s]);
-    }
-    mma_commit(tmem_full);
-  }
-  __syncwarp();
-
-  // epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
-  mbar_wait(tmem_full, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = m0 + warp * 32 + lane;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 8) {
-    uint32_t r[8];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
-      float* out = C + (long long)row * N + n0 + c0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (n0 + c0 + i < N) out[i] = __uint_as_float(r[i]);
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
-  }
-}
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -228,8 +119,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //                  epilogue drains tile i
 //   warps 2-5    : epilogue; warp w reads TMEM lane quarter (w % 4)
 // mbarriers: full/empty per smem stage; acc_full/acc_empty per TMEM buffer.
-// The MMA sequence per tile is the one of gemm_tc_kernel, so the results are
-// bit-identical to it.
+// Per tile the MMA sequence (3 passes x k-steps, in k order) is fixed, so a
+// result does not depend on the tile schedule or the operand majorness.
 // AMN / BMN: operand stored MN-major (the GEMM's M / N index contiguous,
 // e.g. A = cols^T of a weight-gradient GEMM read straight from cols): it is
 // loaded as 32x32 boxes and described with sw128_mn_desc, so no transposed
