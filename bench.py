@@ -416,6 +416,16 @@ def extras(sf, np, _native, plugins, l2hmc):
     from paper_1903_01855_b200.workloads import microbench
 
     out = {}
+    # C3: the chain sweep 10 .. 1e5 (staged, one GPU; at N GPUs each shards
+    # its own chains with no collective, see the headline)
+    c3 = {}
+    sf.init_runtime(sf.RuntimeOptions(seed=3))
+    plugins.install()
+    for b in (10, 100, 1000, 10000, 100000):
+        s = l2hmc.L2HMCSampler(sf, b, "staged", seed=0)
+        dt = _time_steps(s.step, 30, _native)
+        c3[str(b)] = {"samples_per_sec": b / dt, "us_per_transition": dt * 1e6}
+    out["c3_l2hmc_chain_sweep"] = c3
     # C1: L2HMC 200 chains, staged vs eager
     c1 = {}
     for mode, n in (("staged", 50), ("eager", 3)):
