@@ -6,7 +6,11 @@
 // compiled for sm_100a with the same IEEE flags as the AOT kernels, so a
 // fused chain reproduces the eager per-op results bit-for-bit.
 #include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 
 #include "sf_internal.h"
@@ -26,7 +30,96 @@ static std::mutex g_jit_mu;
 static std::unordered_map<std::string, std::unique_ptr<JitKernel>> g_jit_cache;
 static thread_local std::string t_jit_log;
 
+// Persistent compile cache: cubins are stored on disk under
+// $SF_JIT_CACHE (default ~/.cache/paper_1903_01855_b200/jit; "0" disables),
+// keyed by a 64-bit FNV-1a hash of the kernel name, the generated source, the
+// embedded sf_ops.cuh and the NVRTC version, and re-checked against the full
+// key stored in the file, so a later process skips NVRTC for every graph it
+// has lowered before.
+static std::string cache_dir() {
+  const char* env = getenv("SF_JIT_CACHE");
+  if (env && std::string(env) == "0") return "";
+  if (env && *env) return env;
+  const char* home = getenv("HOME");
+  return home ? std::string(home) + "/.cache/paper_1903_01855_b200/jit" : "";
+}
+
+static uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+// the IEEE flags of the AOT kernels (Makefile), so fused code matches eager bits
+static const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "-prec-div=true",
+                                   "-prec-sqrt=true", "-ftz=false", "-default-device",
+                                   "-std=c++17", "-lineinfo", "-DSF_JIT=1"};
+
+static std::string cache_key(const std::string& name, const std::string& src) {
+  int major = 0, minor = 0;
+  nvrtcVersion(&major, &minor);
+  std::string opts;
+  for (const char* o : kNvrtcOpts) opts += std::string(o) + ' ';
+  return name + '\n' + std::to_string(major) + "." + std::to_string(minor) + '\n' + opts + '\n' +
+         std::to_string(fnv1a(kSfOpsCuh)) + '\n' + src;
+}
+
+static std::string cache_path(const std::string& key) {
+  const std::string dir = cache_dir();
+  if (dir.empty()) return "";
+  char buf[32];
+  snprintf(buf, sizeof(buf), "%016llx", (unsigned long long)fnv1a(key));
+  return dir + "/" + buf + ".cubin";
+}
+
+static bool cache_load(const std::string& key, std::vector<char>* cubin) {
+  const std::string path = cache_path(key);
+  if (path.empty()) return false;
+  FILE* f = fopen(path.c_str(), "rb");
+  if (!f) return false;
+  uint64_t klen = 0, clen = 0;
+  bool ok = fread(&klen, 8, 1, f) == 1 && klen == key.size();
+  std::string stored(ok ? klen : 0, '\0');
+  ok = ok && fread(&stored[0], 1, klen, f) == klen && stored == key &&
+       fread(&clen, 8, 1, f) == 1 && clen > 0 && clen < (1ull << 30);
+  if (ok) {
+    cubin->resize(clen);
+    ok = fread(cubin->data(), 1, clen, f) == clen;
+  }
+  fclose(f);
+  return ok;
+}
+
+static void cache_store(const std::string& key, const std::vector<char>& cubin) {
+  const std::string path = cache_path(key);
+  if (path.empty()) return;
+  std::string cmd_dir = cache_dir();
+  // mkdir -p, one component at a time
+  for (size_t i = 1; i <= cmd_dir.size(); ++i)
+    if (i == cmd_dir.size() || cmd_dir[i] == '/') mkdir(cmd_dir.substr(0, i).c_str(), 0755);
+  const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)getpid());
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const uint64_t klen = key.size(), clen = cubin.size();
+  bool ok = fwrite(&klen, 8, 1, f) == 1 && fwrite(key.data(), 1, klen, f) == klen &&
+            fwrite(&clen, 8, 1, f) == 1 && fwrite(cubin.data(), 1, clen, f) == clen;
+  ok = (fclose(f) == 0) && ok;
+  if (ok) rename(tmp.c_str(), path.c_str());  // atomic publish
+  else remove(tmp.c_str());
+}
+
+static int compile_nvrtc(const std::string& name, const std::string& src,
+                         std::vector<char>* cubin);
+
 static int compile(const std::string& name, const std::string& src, std::vector<char>* cubin) {
+  const std::string key = cache_key(name, src);
+  if (cache_load(key, cubin)) return SF_OK;
+  SF_TRY(compile_nvrtc(name, src, cubin));
+  cache_store(key, *cubin);
+  return SF_OK;
+}
+
+static int compile_nvrtc(const std::string& name, const std::string& src,
+                         std::vector<char>* cubin) {
   nvrtcProgram prog;
   const char* headers[] = {kSfOpsCuh};
   const char* header_names[] = {"sf_ops.cuh"};
@@ -36,10 +129,7 @@ static int compile(const std::string& name, const std::string& src, std::vector<
     set_error(std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
     return SF_ERR_NVRTC;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false",     "-prec-div=true",
-                        "-prec-sqrt=true",            "-ftz=false",      "-default-device",
-                        "-std=c++17",                 "-lineinfo",       "-DSF_JIT=1"};
-  r = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  r = nvrtcCompileProgram(prog, (int)(sizeof(kNvrtcOpts) / sizeof(kNvrtcOpts[0])), kNvrtcOpts);
   size_t log_size = 0;
   nvrtcGetProgramLogSize(prog, &log_size);
   t_jit_log.assign(log_size, '\0');

@@ -54,6 +54,29 @@ def test_jit_compiles_generated_kernel_without_gpu():
     assert _native.jit_compile("k_test", src) != 0
 
 
+def test_jit_disk_cache_across_processes(tmp_path):
+    """The NVRTC cubin cache (sf_jit.cpp) persists across processes and
+    ignores a corrupted entry."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1903_01855_b200 import _native\n"
+            "src = '#include \"sf_ops.cuh\"\\nextern \"C\" __global__ void k_cache(float* p) "
+            "{ p[threadIdx.x] = sf::exp_(p[threadIdx.x]); }'\n"
+            "assert _native.jit_compile('k_cache', src) != 0\n") % ROOT
+    env = dict(os.environ, SF_JIT_CACHE=str(tmp_path))
+    subprocess.run([sys.executable, "-c", code], env=env, check=True)
+    files = sorted(tmp_path.glob("*.cubin"))
+    assert len(files) == 1 and files[0].stat().st_size > 100
+    before = files[0].stat().st_mtime_ns
+    subprocess.run([sys.executable, "-c", code], env=env, check=True)  # served from disk
+    assert files[0].stat().st_mtime_ns == before
+    files[0].write_bytes(b"garbage")                                   # corrupted: recompiled
+    subprocess.run([sys.executable, "-c", code], env=env, check=True)
+    assert files[0].stat().st_size > 100
+
+
 # ---------------------------------------------------------------- tensors / dtypes
 def test_tensor_from_host_checks():
     t = sf.tensor_from_host([2.0, -2.0], (2, 1), sf.float32)
@@ -207,6 +230,26 @@ def test_serialization_round_trip_and_errors():
         deserialize(b"XXXX" + blob[4:])
     with pytest.raises(CorruptGraph):
         deserialize(blob[: len(blob) // 2])
+
+
+def test_deserialize_plugin_ops_through_the_registry():
+    """the reference's deserialize infers node specs from a
+    global table and cannot load plugin ops (stageflow/serial.py:397); here
+    inference goes through the live registry, so a registered plugin op
+    round-trips."""
+    from paper_1903_01855_b200 import plugins
+
+    plugins.install()
+    b = GraphBuilder()
+    x = b.add_placeholder("x", sf.float32, (4,))
+    (y,) = b.add_node("tanh", [x], {}, None, [(sf.float32, (4,))])
+    (z,) = b.add_node("select", [b.add_node("greater", [y, x], {}, None,
+                                            [(sf.boolean, (4,))])[0], y, x], {}, None,
+                      [(sf.float32, (4,))])
+    gf = b.finalize("plug", [z], ["z"])
+    blob = serialize(gf)
+    back = deserialize(blob)
+    assert serialize(back) == blob and [n.op for n in back.nodes] == ["tanh", "greater", "select"]
 
 
 # ---------------------------------------------------------------- tapes (lifecycle only)
