@@ -647,6 +647,9 @@ class _Gen:
             size = (n // N) * Np
         else:
             off, pidx, size = "q", list(range(n)), n
+        if width in (4, 8):
+            vw = 16 // width  # slices start 16-byte aligned; vector reads stay inside
+            size = -(-size // vw) * vw
         self.smem.append(f"  __shared__ __align__(16) {ct} {name}[{max(1, size * len(slots))}];")
         head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= 128 else
                 f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) ")
@@ -931,6 +934,30 @@ class _Gen:
             off //= 2
         return acc[0]
 
+    def _vector_operands(self, op: LOp, w: int, lines: List[str]) -> Dict[int, List[str]]:
+        """A row-wide uniform operand of an elementwise op (a bias, a scale
+        vector) read with 16-byte vector loads instead of one load per
+        element: operand index -> element expressions."""
+        out: Dict[int, List[str]] = {}
+        if w < 2:
+            return out
+        for q, x in enumerate(op.ins):
+            r = x.root()
+            if (self.P.layout_of(x)[0] != UNI or x.numel != w or r.numel != w
+                    or id(r) not in self.smem_name or id(r) in self.pad
+                    or r.dtype.width not in (4, 8)):
+                continue
+            name, base = self.smem_name[id(r)]
+            vw = 16 // r.dtype.width
+            vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
+            elems = []
+            for g in range(0, w, vw):
+                t = self._new_tmp()
+                lines.append(f"const {vt} {t} = {ld}(&{name}[{base}{g}]);")
+                elems += [f"{t}.{c}" for c in "xyzw"[:min(vw, w - g)]]
+            out[q] = elems
+        return out
+
     def _emit_rowed(self, op: LOp, L) -> None:
         _, w, rank = L
         o = op.outs[0]
@@ -941,10 +968,12 @@ class _Gen:
         lines = []
         k = op.kind
         if k == "ew":
+            vec = self._vector_operands(op, w, lines)
             for j in range(w):
                 for rep in range(self.R):
                     self.rep = rep
-                    args = [self.row_elem(x, j, w, rank) for x in op.ins]
+                    args = [vec[q][j] if q in vec else self.row_elem(x, j, w, rank)
+                            for q, x in enumerate(op.ins)]
                     lines.append(f"const {ct} {per_rep[rep][j]} = {ew_expr(op.name, args, ct)};")
         elif k == "matmul":
             a, b = op.ins
