@@ -324,4 +324,55 @@ SF_DEVFN double2 lds2(const double* p) {
   return v;
 }
 
+// Same loads from a row program's shared-memory pool: base register + a
+// compile-time byte offset, so the address folds into the LDS instruction
+// (no per-load integer add).
+template <class T, int OFF> struct PoolLd;
+template <int OFF> struct PoolLd<float, OFF> {
+  static SF_DEVFN float ld(unsigned b) {
+    float v;
+    asm volatile("ld.volatile.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(b), "n"(OFF));
+    return v;
+  }
+};
+template <int OFF> struct PoolLd<double, OFF> {
+  static SF_DEVFN double ld(unsigned b) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(b), "n"(OFF));
+    return v;
+  }
+};
+template <int OFF> struct PoolLd<int, OFF> {
+  static SF_DEVFN int ld(unsigned b) {
+    int v;
+    asm volatile("ld.volatile.shared.s32 %0, [%1+%2];" : "=r"(v) : "r"(b), "n"(OFF));
+    return v;
+  }
+};
+template <int OFF> struct PoolLd<bool, OFF> {
+  static SF_DEVFN bool ld(unsigned b) {
+    unsigned short v;
+    asm volatile("ld.volatile.shared.u8 %0, [%1+%2];" : "=h"(v) : "r"(b), "n"(OFF));
+    return v != 0;
+  }
+};
+template <class T, int OFF>
+SF_DEVFN T ldp(unsigned b) { return PoolLd<T, OFF>::ld(b); }
+template <int OFF>
+SF_DEVFN float4 ldp4(unsigned b) {
+  float4 v;
+  asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(b), "n"(OFF));
+  return v;
+}
+template <int OFF>
+SF_DEVFN double2 ldp2(unsigned b) {
+  double2 v;
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2+%3];"
+               : "=d"(v.x), "=d"(v.y)
+               : "r"(b), "n"(OFF));
+  return v;
+}
+
 }  // namespace sf

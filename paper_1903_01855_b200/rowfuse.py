@@ -527,8 +527,12 @@ class _Gen:
         # (Np = N rounded up to one 16-byte vector) so a weight row is one or
         # a few vector loads: root id -> (N, Np)
         self.pad: Dict[int, Tuple[int, int]] = {}
-        # root id -> (shared array, base-offset expression) of staged operands
-        self.smem_name: Dict[int, Tuple[str, str]] = {}
+        # root id -> (pool array name, stacked per loop iteration?) of staged operands
+        self.smem_name: Dict[int, Tuple[str, bool]] = {}
+        # row kernels: the shared-memory pool (array -> (byte offset, slice
+        # elements, C type, element width)) and its size in bytes
+        self.pool: Dict[str, Tuple[int, int, str, int]] = {}
+        self.pool_size = 0
         # uniform kernel: staged global operands, CSE table, aliased results
         self.staged: Dict[int, str] = {}
         self.uni_smem = _uniform_smem(rp) if rp.uniform_only else 0
@@ -592,8 +596,8 @@ class _Gen:
                     and id(r) not in self.uni_names):
                 # slot taken by a loop's stacked operand; stage it on its own too
                 pidx, _ = self._stage(r, f"s{k}", [k])
-                self.uni_names[id(r)] = [f"sf::lds(&s{k}[{p}])" for p in pidx]
-                self.smem_name[id(r)] = (f"s{k}", "")
+                self.uni_names[id(r)] = [self._lds(f"s{k}", p, False) for p in pidx]
+                self.smem_name[id(r)] = (f"s{k}", False)
             return
         k = len(self.ext)
         self.ptr_of[id(r)] = k
@@ -630,8 +634,8 @@ class _Gen:
         else:
             self.ext_kind.append(UNI)
             pidx, _ = self._stage(r, f"s{k}", [k])
-            self.uni_names[id(r)] = [f"sf::lds(&s{k}[{p}])" for p in pidx]
-            self.smem_name[id(r)] = (f"s{k}", "")
+            self.uni_names[id(r)] = [self._lds(f"s{k}", p, False) for p in pidx]
+            self.smem_name[id(r)] = (f"s{k}", False)
 
     def _stage(self, r: LV, name: str, slots: List[int]):
         """Stage uniform operand(s) of r's shape into shared array ``name``
@@ -650,16 +654,34 @@ class _Gen:
         if width in (4, 8):
             vw = 16 // width  # slices start 16-byte aligned; vector reads stay inside
             size = -(-size // vw) * vw
-        self.smem.append(f"  __shared__ __align__(16) {ct} {name}[{max(1, size * len(slots))}];")
+        # one pool per kernel: every array is a fixed byte offset from one base
+        # register, so each load is LDS [base + immediate]
+        pos = -(-self.pool_size // 16) * 16
+        self.pool[name] = (pos, size, ct, width)
+        self.pool_size = pos + max(1, size * len(slots)) * width
         head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= 128 else
                 f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) ")
         for i, k in enumerate(slots):
-            dst = f"{name}[{i * size} + {off}]" if i else f"{name}[{off}]"
+            dst = f"smem_pool + {pos + i * size * width} + {width} * ({off})"
             src_q = f"((const {ct}*)a.p[{k}])[q]"
-            copy = (f"sf::cp_async<{width}>(&{dst}, &{src_q});" if width in (4, 8)
-                    else f"{dst} = {src_q};")
+            copy = (f"sf::cp_async<{width}>({dst}, &{src_q});" if width in (4, 8)
+                    else f"*({ct}*)({dst}) = {src_q};")
             self.smem.append(f"  {head}{copy}")
         return pidx, size
+
+    def _lds(self, name: str, index: int, stacked: bool) -> str:
+        """Scalar load of element ``index`` of pool array ``name`` (of the
+        current loop iteration's slice when stacked)."""
+        pos, size, ct, width = self.pool[name]
+        base = f"(sp + it * {size * width})" if stacked else "sp"
+        return f"sf::ldp<{ct}, {pos + index * width}>({base})"
+
+    def _lds_vec(self, name: str, index: int, stacked: bool) -> str:
+        """16-byte vector load starting at element ``index`` (aligned)."""
+        pos, size, ct, width = self.pool[name]
+        base = f"(sp + it * {size * width})" if stacked else "sp"
+        fn = "sf::ldp4" if width == 4 else "sf::ldp2"
+        return f"{fn}<{pos + index * width}>({base})"
 
     def _ext_slot(self, r: LV, kind: str) -> int:
         """Pointer slot of an external root without staging it."""
@@ -866,8 +888,8 @@ class _Gen:
             name = f"S{syn.id}"
             slots = [self._ext_slot(r, UNI) for r in roots]
             pidx, size = self._stage(syn, name, slots)
-            self.uni_names[id(syn)] = [f"sf::lds(&{name}[it * {size} + {p}])" for p in pidx]
-            self.smem_name[id(syn)] = (name, f"it * {size} + ")
+            self.uni_names[id(syn)] = [self._lds(name, p, True) for p in pidx]
+            self.smem_name[id(syn)] = (name, True)
         pre = []
         for syn, init, _src in lp.carried:
             _, w, rank = self.P.layout_of(syn)
@@ -947,13 +969,13 @@ class _Gen:
                     or id(r) not in self.smem_name or id(r) in self.pad
                     or r.dtype.width not in (4, 8)):
                 continue
-            name, base = self.smem_name[id(r)]
+            name, stacked = self.smem_name[id(r)]
             vw = 16 // r.dtype.width
-            vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
+            vt = "float4" if vw == 4 else "double2"
             elems = []
             for g in range(0, w, vw):
                 t = self._new_tmp()
-                lines.append(f"const {vt} {t} = {ld}(&{name}[{base}{g}]);")
+                lines.append(f"const {vt} {t} = {self._lds_vec(name, g, stacked)};")
                 elems += [f"{t}.{c}" for c in "xyzw"[:min(vw, w - g)]]
             out[q] = elems
         return out
@@ -994,9 +1016,9 @@ class _Gen:
                 # n accumulators advance together (same sequential-k FMA chain
                 # per output as the nested form / the eager kernel)
                 N, Np = self.pad[id(br)]
-                sname, sbase = self.smem_name[id(br)]
+                sname, stacked = self.smem_name[id(br)]
                 vw = 16 // br.dtype.width
-                vt, ld = ("float4", "sf::lds4") if vw == 4 else ("double2", "sf::lds2")
+                vt = "float4" if vw == 4 else "double2"
                 comp = "xyzw"
                 lines.append(" ".join(f"{ct} {nm} = ({ct})0;" for names in per_rep
                                       for nm in names))
@@ -1018,7 +1040,7 @@ class _Gen:
                     while issued < min(limit, len(order)):
                         v = order[issued]
                         t = self._new_tmp()
-                        stmt.append(f"const {vt} {t} = {ld}(&{sname}[{sbase}{v * vw}]);")
+                        stmt.append(f"const {vt} {t} = {self._lds_vec(sname, v * vw, stacked)};")
                         vecs[v] = t
                         issued += 1
 
@@ -1124,6 +1146,9 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
            "__grid_constant__ Params a) {"]
     loads = [x for x in g.smem if "int q" in x]
     decls = [x for x in g.smem if "int q" not in x]
+    if g.pool_size:
+        decls.append(f"  __shared__ __align__(16) unsigned char smem_pool[{g.pool_size}];\n"
+                     "  const unsigned sp = sf::saddr(smem_pool);")
     src += decls + loads
     if loads:
         src.append("  sf::cp_wait();\n  __syncthreads();")
