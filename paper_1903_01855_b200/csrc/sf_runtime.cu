@@ -344,6 +344,19 @@ int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes) {
     SF_CHECK_CUDA(cudaEventRecord(d->slot_ready[k], d->stream));
     return SF_OK;
   }
+  {
+    // pinned source and an idle stream: DMA straight from the caller's buffer
+    // and wait for just that copy (the buffer must be free on return) —
+    // saves the host memcpy into the bounce buffer
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+        cudaStreamQuery(d->stream) == cudaSuccess) {
+      SF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, d->stream));
+      SF_CHECK_CUDA(cudaStreamSynchronize(d->stream));
+      return SF_OK;
+    }
+    (void)cudaGetLastError();  // clear cudaErrorNotReady from the query
+  }
   if (bytes <= (256u << 20)) {
     // larger transfers: one pinned bounce buffer, asynchronous w.r.t. the stream
     std::lock_guard<std::mutex> lk(d->stage_mu);
