@@ -68,6 +68,11 @@ int sf_alloc(int dev, size_t bytes, void** p);
 int sf_free(int dev, void* p);
 int sf_mem_stats(int dev, size_t* bytes_in_use, size_t* bytes_cached);
 int sf_trim(int dev);
+/* Page-locked host memory (cudaHostAlloc, portable).  Transfers to/from it
+ * skip the staging copies: sf_memcpy_d2h writes it directly, sf_memcpy_h2d
+ * reads it directly when the stream is idle. */
+int sf_host_alloc(size_t bytes, void** p);
+int sf_host_free(void* p);
 
 /* host <-> device copies.  h2d copies the host bytes before returning (the
  * caller may reuse `src` immediately); d2h blocks until the data is on the

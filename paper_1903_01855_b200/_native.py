@@ -61,6 +61,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_mem_stats": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
                                          ctypes.POINTER(ctypes.c_size_t)]),
         "sf_trim": (ctypes.c_int, [ctypes.c_int]),
+        "sf_host_alloc": (ctypes.c_int, [ctypes.c_size_t, _PVP]),
+        "sf_host_free": (ctypes.c_int, [_VP]),
         "sf_memcpy_h2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_d2h": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_d2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
@@ -130,6 +132,7 @@ def _declare(lib: ctypes.CDLL) -> None:
 EXPORTED_SYMBOLS = (
     "sf_last_error", "sf_version", "sf_init", "sf_device_info", "sf_set_stream",
     "sf_get_stream", "sf_device_sync", "sf_alloc", "sf_free", "sf_mem_stats", "sf_trim",
+    "sf_host_alloc", "sf_host_free",
     "sf_memcpy_h2d", "sf_memcpy_d2h", "sf_memcpy_d2d", "sf_memcpy_p2p", "sf_elementwise",
     "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
@@ -312,7 +315,78 @@ def upload(dev: int, arr: np.ndarray) -> DeviceBuffer:
     return buf
 
 
+class _PinnedBlock:
+    """A page-locked host block; returns itself to the pool when the numpy
+    array built over it is collected."""
+
+    __slots__ = ("ptr", "cap")
+
+    def __init__(self, ptr: int, cap: int):
+        self.ptr, self.cap = ptr, cap
+
+    def __del__(self):
+        try:
+            _PINNED.put(self)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class _PinnedPool:
+    """Size-class pool of page-locked host blocks for device->host results:
+    the DMA lands directly in the array the caller receives (no staging
+    copy).  At most LIMIT bytes stay cached."""
+
+    LIMIT = 256 << 20
+    MIN = 64 << 10
+    MAX_ARRAY = 64 << 20  # larger results use pageable memory (page-locking is scarce)
+
+    def __init__(self):
+        self.free: dict = {}
+        self.cached = 0
+        self.lock = threading.Lock()
+
+    def get(self, nbytes: int) -> Optional["_PinnedBlock"]:
+        cap = self.MIN
+        while cap < nbytes:
+            cap <<= 1
+        with self.lock:
+            lst = self.free.get(cap)
+            if lst:
+                self.cached -= cap
+                return _PinnedBlock(lst.pop(), cap)
+        p = ctypes.c_void_p(0)
+        if _lib.sf_host_alloc(cap, ctypes.byref(p)):
+            return None
+        return _PinnedBlock(p.value, cap)
+
+    def put(self, blk: "_PinnedBlock") -> None:
+        ptr, blk.ptr = blk.ptr, 0
+        if not ptr:
+            return
+        with self.lock:
+            if self.cached + blk.cap <= self.LIMIT:
+                self.free.setdefault(blk.cap, []).append(ptr)
+                self.cached += blk.cap
+                return
+        _lib.sf_host_free(ptr)
+
+
+_PINNED = _PinnedPool()
+
+
 def download(buf: DeviceBuffer, np_dtype, shape) -> np.ndarray:
+    nbytes = int(np.prod(shape, dtype=np.int64)) * np.dtype(np_dtype).itemsize
+    if _PinnedPool.MIN <= nbytes <= _PinnedPool.MAX_ARRAY:
+        blk = _PINNED.get(nbytes)
+        if blk is not None:
+            # the array lives in page-locked memory: the copy DMAs straight into it
+            cbuf = (ctypes.c_char * nbytes).from_address(blk.ptr)
+            cbuf._blk = blk  # the block is freed to the pool with the array
+            out = np.frombuffer(cbuf, dtype=np_dtype).reshape(shape)
+            rc = _lib.sf_memcpy_d2h(buf.dev, blk.ptr, buf.ptr, nbytes)
+            if rc:
+                raise _err(_lib, rc, "sf_memcpy_d2h")
+            return out
     out = np.empty(shape, dtype=np_dtype)
     if out.nbytes:
         rc = _lib.sf_memcpy_d2h(buf.dev, out.ctypes.data, buf.ptr, out.nbytes)

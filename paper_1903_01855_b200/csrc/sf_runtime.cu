@@ -326,6 +326,18 @@ int sf_trim(int dev) {
   return d->alloc.trim();
 }
 
+int sf_host_alloc(size_t bytes, void** p) {
+  int n = 0;
+  SF_TRY(sf_init(&n));
+  SF_CHECK_CUDA(cudaHostAlloc(p, bytes ? bytes : 1, cudaHostAllocPortable));
+  return SF_OK;
+}
+
+int sf_host_free(void* p) {
+  if (p) SF_CHECK_CUDA(cudaFreeHost(p));
+  return SF_OK;
+}
+
 int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes) {
   if (bytes == 0) return SF_OK;
   Device* d;
@@ -386,8 +398,13 @@ int sf_memcpy_d2h(int dev, void* dst, const void* src, size_t bytes) {
     SF_CHECK_CUDA(cudaStreamSynchronize(d->stream));
     return SF_OK;
   }
-  if (bytes >= (64u << 10) && bytes <= (256u << 20)) {
+  cudaPointerAttributes attr;
+  const bool pinned_dst =
+      cudaPointerGetAttributes(&attr, dst) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+  (void)cudaGetLastError();
+  if (bytes >= (64u << 10) && bytes <= (256u << 20) && !pinned_dst) {
     // DMA into a pinned bounce buffer at full PCIe/C2C speed, then one memcpy
+    // (a pinned destination, e.g. sf_host_alloc memory, is written directly)
     std::lock_guard<std::mutex> lk(d->d2h_mu);
     if (d->pinned_d2h_bytes < bytes) {
       if (d->pinned_d2h) cudaFreeHost(d->pinned_d2h);
