@@ -598,8 +598,7 @@ class NativePlan:
     def run(self, in_ptrs: Sequence[int]) -> List[int]:
         with self._lock:
             arr = self._in_arr
-            for i, p in enumerate(in_ptrs):
-                arr[i] = p
+            arr[:len(in_ptrs)] = in_ptrs  # one slice store (per-item stores cost ~0.15 us each)
             outs = self._out_arr
             rc = _lib.sf_plan_run(self.handle, arr, outs)
             if rc:

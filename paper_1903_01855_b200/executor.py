@@ -455,7 +455,46 @@ class Program:
             self._replayable_flag = r
         return r
 
+    def _single_plan(self):
+        """(plan, input positions, output specs) when the whole program is one
+        native plan whose outputs are all plan outputs; False otherwise."""
+        segs = self.segments
+        if len(segs) != 1 or not isinstance(segs[0], _NativeSegment):
+            return False
+        seg = segs[0]
+        pos = {id(lv.root()): i for i, lv in enumerate(self.in_vals)}
+        if any(id(r) not in pos for r in seg.in_roots):
+            return False
+        slot = {id(r): (j, r.nbytes) for j, r in enumerate(seg.out_roots)}
+        outs = []
+        for lv in self.out_vals:
+            s = slot.get(id(lv.root()))
+            if s is None:
+                return False
+            outs.append((s[0], s[1], lv.dtype, lv.shape))
+        if len({j for j, _, _, _ in outs}) != len(outs) or len(outs) != len(seg.out_roots):
+            return False  # an output returned twice (or unused) shares one buffer
+        return seg.plan, [pos[id(r)] for r in seg.in_roots], outs
+
     def _run_direct(self, inputs: Sequence, libraries) -> List[Tensor]:
+        fast = self.__dict__.get("_fast")
+        if fast is None:
+            fast = self._fast = self._single_plan()
+        if fast:
+            plan, pos, specs = fast
+            ptrs = []
+            for i in pos:
+                h = inputs[i]
+                if type(h) is Tensor:
+                    b = h._buf
+                    ptrs.append(b.ptr if b is not None else h._ptr())
+                elif isinstance(h, Tensor):
+                    ptrs.append(h._ptr())
+                else:
+                    ptrs.append(h._storage_ptr())  # Variable
+            raw = plan.run(ptrs)
+            dev, device, DB, adopt = self.dev, self.device, _native.DeviceBuffer, Tensor._adopt
+            return [adopt(dt, shape, device, DB(dev, raw[j], nb)) for j, nb, dt, shape in specs]
         env: Dict[int, object] = {}
         for lv, v in zip(self.in_vals, inputs):
             env[id(lv)] = v
