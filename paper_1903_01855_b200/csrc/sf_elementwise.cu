@@ -7,6 +7,8 @@
 // tensor-with-scalar) take a vectorised 128-bit path with no index math.
 // Scalar operands that the front-end knows on the host travel as immediates
 // in the launch parameters instead of through an H2D copy.
+#include <type_traits>
+
 #include "sf_internal.h"
 #include "sf_ops.cuh"
 
@@ -78,6 +80,56 @@ __global__ void ew_2d(const EwArgs a, O* __restrict__ out) {
     const T y = a.n_in > 1 ? fetch<T>(a, 1, (long long)(r * s10 + c * s11)) : x;
     out[i] = apply<T, O>(a.op, x, y);
   }
+}
+
+// Two collapsed dims, float32, cols % 4 == 0: each thread produces 4
+// consecutive elements of one row.  An operand is a row-contiguous matrix
+// (inner stride 1: one 16-byte load), a per-row value (inner stride 0: one
+// scalar load shared by the 4 lanes), or an immediate.  The per-channel
+// vectors of NHWC activations stay in L1/L2, so HBM sees one read per
+// activation operand and one write.
+__device__ __forceinline__ float4 fetch4(const EwArgs& a, int j, unsigned r, unsigned c) {
+  const float* p = (const float*)a.in[j];
+  if (!p) {
+    const float v = (float)a.imm[j];
+    return make_float4(v, v, v, v);
+  }
+  const unsigned s0 = (unsigned)a.strides[j][0];
+  if (a.strides[j][1] == 0) {
+    const float v = p[r * s0];
+    return make_float4(v, v, v, v);
+  }
+  return *reinterpret_cast<const float4*>(p + r * s0 + c);
+}
+
+__global__ void __launch_bounds__(256) ew_2d_f32x4(const EwArgs a, float* __restrict__ out) {
+  const unsigned n4 = (unsigned)(a.n >> 2), cols = (unsigned)a.shape[1];
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const unsigned e = i << 2, r = e / cols, c = e - r * cols;
+    const float4 x = fetch4(a, 0, r, c);
+    const float4 y = a.n_in > 1 ? fetch4(a, 1, r, c) : x;
+    float4 o;
+    o.x = apply<float, float>(a.op, x.x, y.x);
+    o.y = apply<float, float>(a.op, x.y, y.y);
+    o.z = apply<float, float>(a.op, x.z, y.z);
+    o.w = apply<float, float>(a.op, x.w, y.w);
+    reinterpret_cast<float4*>(out)[i] = o;
+  }
+}
+
+static bool ew_2d_x4_ok(const EwArgs& a, const void* out) {
+  if (a.ndim != 2 || a.shape[1] % 4 != 0 || a.n >= (1LL << 32) || (uintptr_t)out % 16) return false;
+  for (int j = 0; j < a.n_in; ++j) {
+    if (!a.in[j]) continue;
+    if (a.strides[j][1] == 1) {
+      if (a.strides[j][0] % 4 || (uintptr_t)a.in[j] % 16) return false;
+    } else if (a.strides[j][1] != 0) {
+      return false;
+    }
+    if (a.shape[0] * (a.strides[j][0] + 1) >= (1LL << 32)) return false;
+  }
+  return true;
 }
 
 // Flat path: every operand is either full-size contiguous or a scalar.
@@ -212,6 +264,9 @@ template <class T, class O>
 static void dispatch_ew(Device* d, const EwArgs& a, void* out, bool flat) {
   if (flat) {
     ew_flat<T, O><<<grid_for(d, a.n), 256, 0, d->stream>>>(a, (O*)out);
+  } else if (std::is_same<T, float>::value && std::is_same<O, float>::value &&
+             ew_2d_x4_ok(a, out)) {
+    ew_2d_f32x4<<<grid_for(d, a.n / 4), 256, 0, d->stream>>>(a, (float*)out);
   } else if (a.ndim == 2 && a.n < (1LL << 31) &&
              a.shape[0] * (a.strides[0][0] + a.strides[1][0] + 1) < (1LL << 31)) {
     ew_2d<T, O><<<grid_for(d, a.n), 256, 0, d->stream>>>(a, (O*)out);

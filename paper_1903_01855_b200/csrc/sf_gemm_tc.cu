@@ -323,6 +323,52 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict
   }
 }
 
+// Same split with 16-byte accesses, two vectors in flight per thread and
+// iteration (HBM-bound: 4 B read + 4 B written per element when hi is skipped).
+__device__ __forceinline__ float4 tf32_lo4(float4 v, float4* h) {
+  const unsigned m = 0xFFFFE000u;
+  h->x = __uint_as_float(__float_as_uint(v.x) & m);
+  h->y = __uint_as_float(__float_as_uint(v.y) & m);
+  h->z = __uint_as_float(__float_as_uint(v.z) & m);
+  h->w = __uint_as_float(__float_as_uint(v.w) & m);
+  return make_float4(v.x - h->x, v.y - h->y, v.z - h->z, v.w - h->w);
+}
+
+__global__ void __launch_bounds__(256) split_tf32_x4_kernel(const float* __restrict__ x,
+                                                            float* __restrict__ hi,
+                                                            float* __restrict__ lo, long long n) {
+  const long long n4 = n >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4* lo4 = reinterpret_cast<float4*>(lo);
+  float4* hi4 = reinterpret_cast<float4*>(hi);
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + stride < n4; i += 2 * stride) {
+    const float4 a = x4[i], b = x4[i + stride];
+    float4 ha, hb;
+    const float4 la = tf32_lo4(a, &ha), lb = tf32_lo4(b, &hb);
+    lo4[i] = la;
+    lo4[i + stride] = lb;
+    if (hi) {
+      hi4[i] = ha;
+      hi4[i + stride] = hb;
+    }
+  }
+  for (; i < n4; i += stride) {
+    float4 h;
+    lo4[i] = tf32_lo4(x4[i], &h);
+    if (hi) hi4[i] = h;
+  }
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long j = (n4 << 2) + t;
+  if (t < 4 && j < n) {
+    const float v = x[j];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    if (hi) hi[j] = h;
+    lo[j] = v - h;
+  }
+}
+
 // (R x Cc) row-major -> hi/lo of its transpose (Cc x ldo), rows padded to ldo
 __global__ void split_tf32_transpose_kernel(const float* __restrict__ x, float* __restrict__ hi,
                                             float* __restrict__ lo, long long R, long long Cc,
@@ -461,6 +507,14 @@ int launch_gemm_tc(Device* d, int64_t M, int64_t N, int64_t K, const float* ahi,
 
 int launch_split_tf32(Device* d, int64_t n, const float* x, float* hi, float* lo) {
   if (n == 0) return SF_OK;
+  if (((uintptr_t)x | (uintptr_t)hi | (uintptr_t)lo) % 16 == 0 && n >= 4096) {
+    long long blocks = (n / 4 + 255) / 256;
+    if (blocks > d->sm_count * 8LL) blocks = d->sm_count * 8LL;
+    split_tf32_x4_kernel<<<(unsigned)blocks, 256, 0, d->stream>>>(x, hi, lo, n);
+    count_launch(d->id);
+    SF_CHECK_CUDA(cudaGetLastError());
+    return SF_OK;
+  }
   long long blocks = (n + 255) / 256;
   if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
   split_tf32_kernel<<<(unsigned)blocks, 256, 0, d->stream>>>(x, hi, lo, n);

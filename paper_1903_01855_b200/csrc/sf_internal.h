@@ -118,6 +118,11 @@ struct Device {
   char* pinned_d2h = nullptr;
   size_t pinned_d2h_bytes = 0;
   int sm_count = 0;
+  // arrival counters of single-launch multi-chunk reductions: zero at rest
+  // (the last block of a column group resets its counter), so one array
+  // serves every launch on the device's stream, graph replays included
+  static constexpr int kRedCounters = 1 << 16;
+  unsigned* red_counters = nullptr;
   // device RNG (Philox) state: seed and next counter offset
   unsigned long long rng_seed = 0;
   unsigned long long rng_offset = 0;

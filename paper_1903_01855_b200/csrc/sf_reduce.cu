@@ -10,6 +10,8 @@
 //   i32 sum wraps modulo 2^32 (numpy accumulates in int64, _wrap casts back).
 //   i32 mean (eager only; staged inference rejects it, kernels.py:344-352)
 //   accumulates in f64, divides, truncates to int32 like the astype in _wrap.
+#include <type_traits>
+
 #include "sf_internal.h"
 #include "sf_ops.cuh"
 
@@ -168,6 +170,169 @@ __global__ void __launch_bounds__(1024) reduce_cols(const T* __restrict__ in, lo
     }
     part[c * n_chunks + j] = a[0];
   }
+}
+
+// float32 column reduction with 16-byte loads (C % 4 == 0, 16-byte aligned):
+// thread (tx, l) folds partial lane l of 4 adjacent columns — rows l, l+32,
+// ... of the chunk, left to right, exactly the fold of reduce_cols — and the
+// 32 lane partials of each column are then combined by one warp with the xor
+// butterfly (the same tree; lanes past the chunk's end are absent).
+// XT column-quads per block; loads are issued in batches of 8 per thread.
+template <int XT>
+__global__ void __launch_bounds__(XT * 32) reduce_cols_f32x4(const float* __restrict__ in,
+                                                             long long R, long long C,
+                                                             long long chunk, long long n_chunks,
+                                                             float* __restrict__ part,
+                                                             float* __restrict__ out, int mean,
+                                                             float countf,
+                                                             unsigned* __restrict__ counters) {
+  __shared__ float acc_s[32][XT * 4 + 1];
+  const int tx = threadIdx.x, tl = threadIdx.y;
+  const long long c0 = ((long long)blockIdx.x * XT + tx) * 4;
+  const long long j = blockIdx.y;
+  const long long g0 = j * chunk;
+  long long len = R - g0;
+  if (len > chunk) len = chunk;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c0 < C && tl < len) {
+    const float* p = in + (g0 + tl) * C + c0;
+    const long long step = 32 * C;
+    const int n_rows = (int)((len - tl + 31) / 32);  // rows tl, tl+32, ... < len
+    int q = 0;
+    for (; q + 16 <= n_rows; q += 16) {
+      float4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = *reinterpret_cast<const float4*>(p + (q + u) * step);
+      // the lane's first element starts the fold (not 0 + x: keeps -0.0)
+      if (q == 0) acc = v[0];
+      else {
+        acc.x += v[0].x;
+        acc.y += v[0].y;
+        acc.z += v[0].z;
+        acc.w += v[0].w;
+      }
+#pragma unroll
+      for (int u = 1; u < 16; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+    if (q == 0) {
+      acc = *reinterpret_cast<const float4*>(p);
+      q = 1;
+    }
+#pragma unroll 4
+    for (; q < n_rows; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(p + q * step);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+  }
+  acc_s[tl][tx * 4 + 0] = acc.x;
+  acc_s[tl][tx * 4 + 1] = acc.y;
+  acc_s[tl][tx * 4 + 2] = acc.z;
+  acc_s[tl][tx * 4 + 3] = acc.w;
+  __syncthreads();
+  // warp w combines the lane partials of columns 4w .. 4w+3 of this block
+  const int lin = tl * XT + tx, warp = lin >> 5, lane = lin & 31;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int col = warp * 4 + k;
+    const long long c = (long long)blockIdx.x * XT * 4 + col;
+    float a = acc_s[lane][col];
+    bool present = lane < len;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, a, off);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, off);
+      if (present && op) a = a + ov;
+      else if (op) a = ov;
+      present = present || op;
+    }
+    if (lane == 0 && c < C) {
+      if (n_chunks == 1) out[c] = mean ? a / countf : a;
+      else part[c * n_chunks + j] = a;
+    }
+  }
+  if (n_chunks == 1) return;
+  // Several chunks: the last block to finish a column group folds that
+  // group's chunk partials with the CRO (reduce_partials' order) and applies
+  // the mean — one launch instead of three.
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tx == 0 && tl == 0) {
+    const unsigned prev = atomicAdd(&counters[blockIdx.x], 1u);
+    last = prev == (unsigned)n_chunks - 1;
+    if (last) counters[blockIdx.x] = 0;  // at rest again for the next launch
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long c = (long long)blockIdx.x * XT * 4 + warp * 4 + k;
+    if (c >= C) continue;  // warp-uniform
+    const float* pc = part + c * n_chunks;
+    float a = 0.f;
+    bool present = false;
+    for (long long q = lane; q < n_chunks; q += 32) {
+      const float v = __ldcg(pc + q);
+      a = present ? a + v : v;
+      present = true;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, a, off);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, off);
+      if (present && op) a = a + ov;
+      else if (op) a = ov;
+      present = present || op;
+    }
+    if (lane == 0) out[c] = mean ? a / countf : a;
+  }
+}
+
+template <int XT>
+static void launch_cols_x4(Device* d, const float* in, long long R, long long C, long long chunk,
+                           long long n_chunks, float* part, float* out, int mean, float countf) {
+  dim3 grid((unsigned)((C / 4 + XT - 1) / XT), (unsigned)n_chunks);
+  reduce_cols_f32x4<XT><<<grid, dim3(XT, 32), 0, d->stream>>>(in, R, C, chunk, n_chunks, part,
+                                                              out, mean, countf, d->red_counters);
+}
+
+// One launch: sum (or mean) over the rows of a row-major (R, C) float32
+// matrix into out[C].  Requires C % 4 == 0, 16-byte aligned input and at most
+// Device::kRedCounters column groups.
+static bool cols_x4_ok(Device* d, const float* in, long long R, long long C) {
+  return C % 4 == 0 && (uintptr_t)in % 16 == 0 && C / 4 <= Device::kRedCounters && R > 32 &&
+         C >= 8 && (R + SF_CRO_CHUNK - 1) / SF_CRO_CHUNK < 65536;
+}
+
+static int cols_x4(Device* d, const float* in, long long R, long long C, float* out, int mean,
+                   double count) {
+  const long long chunk = R > SF_CRO_CHUNK ? SF_CRO_CHUNK : R;
+  const long long n_chunks = (R + chunk - 1) / chunk;
+  float* part = nullptr;
+  if (n_chunks > 1) SF_TRY(d->alloc.alloc(d->id, sizeof(float) * C * n_chunks, (void**)&part));
+  const float countf = (float)count;
+  // widest block that still gives every SM several blocks; never narrower
+  // than 8 column quads, so each row a warp touches is 128 contiguous bytes
+  // (narrower blocks split sectors and measured 3-10x slower)
+  const long long target = 4LL * d->sm_count;
+#define SF_COLS(XT) launch_cols_x4<XT>(d, in, R, C, chunk, n_chunks, part, out, mean, countf)
+  if ((C / 128) * n_chunks >= target) SF_COLS(32);
+  else if ((C / 64) * n_chunks >= target) SF_COLS(16);
+  else SF_COLS(8);
+#undef SF_COLS
+  count_launch(d->id);
+  if (part) d->alloc.release(part);  // stream-ordered reuse is safe
+  SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
 }
 
 // Sequential CRO over <= 32 values per output, one thread per output; used
@@ -351,6 +516,10 @@ int launch_reduce(Device* d, int op, int dtype, int ndim, const int64_t* shape,
   const unsigned gf = grid_cap(d, a.n_out);
   switch (dtype) {
     case SF_DTYPE_F32: {
+      const bool columns = a.kept_nd == 1 && a.kept_stride[0] == 1 && a.red_nd == 1 &&
+                           a.red_stride[0] == a.kept_shape[0];
+      if (columns && cols_x4_ok(d, (const float*)in, a.r, a.n_out))
+        return cols_x4(d, (const float*)in, a.r, a.n_out, (float*)out, op != 0, count);
       if (op == 0) {
         SF_TRY(run_reduce<float, float>(d, a, (const float*)in, (float*)out));
       } else {

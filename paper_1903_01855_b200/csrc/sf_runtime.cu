@@ -240,6 +240,8 @@ int sf_init(int* n_devices) {
     SF_CHECK_CUDA(cudaFree(nullptr));  // create the primary context
     SF_CHECK_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     SF_CHECK_CUDA(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, i));
+    SF_CHECK_CUDA(cudaMalloc((void**)&d->red_counters, sizeof(unsigned) * Device::kRedCounters));
+    SF_CHECK_CUDA(cudaMemset(d->red_counters, 0, sizeof(unsigned) * Device::kRedCounters));
     SF_CHECK_CUDA(cudaMallocHost((void**)&d->pinned, Device::kStageSlots * Device::kStageSlotBytes));
     for (int k = 0; k < Device::kStageSlots; ++k)
       SF_CHECK_CUDA(cudaEventCreateWithFlags(&d->slot_ready[k], cudaEventDisableTiming));

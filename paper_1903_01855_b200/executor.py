@@ -274,7 +274,7 @@ class Program:
         in_slots = [use(r) for r in ext]
         out_slots = [define(o) for o in outs]
         n = dtypes.element_count(group.shape)
-        grid = max(1, min((n + 255) // 256, _sm_count(self.dev) * 16))
+        grid = max(1, min((n // group.vec + 255) // 256, _sm_count(self.dev) * 16))
         ptrs = in_slots + out_slots
         payload = struct.pack("<QIIII", kernel, grid, 256, 0, len(ptrs))
         payload += struct.pack("<%di" % len(ptrs), *ptrs)

@@ -262,13 +262,14 @@ def _splat_value(t: Tensor):
 
 
 class FusedGroup:
-    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs")
+    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs", "vec")
 
     def __init__(self, shape):
         self.ops: List[LOp] = []
         self.shape = shape
         self.outs_needed: List[LV] = []
         self.ext_inputs: List[LV] = []
+        self.vec = 1  # elements per thread of the generated kernel
 
 
 _PURE_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "eye"))
@@ -307,25 +308,44 @@ def cse(ops: List[LOp]) -> List[LOp]:
 
 
 def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
-    """Group consecutive elementwise ops sharing one output shape."""
+    """Group elementwise ops sharing one output shape into fused kernels.
+
+    An elementwise op joins the latest group of its shape when every operand
+    is available where that group runs (produced before the group, or inside
+    it); it is then computed at the group's position, which is safe because
+    lowered values are immutable and its consumers all come later.  So the
+    per-channel arithmetic of a normalisation layer, interleaved with the
+    reductions that feed it, still becomes one launch per shape instead of
+    one per op."""
     units: List[Any] = []
-    cur: Optional[FusedGroup] = None
+    produced_at: Dict[int, int] = {}
+    latest: Dict[tuple, int] = {}  # shape -> index of the latest group of that shape
+
+    def record(unit_ops, u):
+        for o_op in unit_ops:
+            for o in getattr(o_op, "outs", ()):
+                produced_at[id(o)] = u
+
     for op in ops:
         if isinstance(op, tuple):  # (RowProgram, planner) from rowfuse.plan_rows
-            cur = None
             units.append(op)
+            record(op[0].ops, len(units) - 1)
             continue
         if op.kind == "ew" and fuse_enabled:
-            shape = op.outs[0].shape
-            if cur is not None and cur.shape == shape:
-                cur.ops.append(op)
+            shape = tuple(op.outs[0].shape)
+            g = latest.get(shape)
+            if g is not None and all(produced_at.get(id(x.root()), -1) <= g for x in op.ins):
+                units[g].ops.append(op)
+                record([op], g)
                 continue
-            cur = FusedGroup(shape)
-            cur.ops.append(op)
-            units.append(cur)
+            grp = FusedGroup(op.outs[0].shape)
+            grp.ops.append(op)
+            units.append(grp)
+            latest[shape] = len(units) - 1
+            record([op], len(units) - 1)
             continue
-        cur = None
         units.append(op)
+        record([op], len(units) - 1)
     return units
 
 
@@ -413,6 +433,93 @@ def _index_expr(src_shape, out_shape, idx: str) -> str:
     return " + ".join(terms) if terms else "0"
 
 
+_VEC4 = {DType.float32: "float4", DType.int32: "int4"}
+
+
+def _vector_width(group: FusedGroup, ext, outs) -> int:
+    """4 when every thread can own 4 consecutive elements of one innermost
+    row: 4-byte dtypes only, innermost extent % 4 == 0, and each external
+    operand either full-shape, row-broadcast (innermost stride 1: one 16-byte
+    load) or column-broadcast (innermost stride 0: one scalar load)."""
+    shape = tuple(group.shape)
+    if not shape or shape[-1] % 4 or dtypes.element_count(shape) < 1024:
+        return 1
+    for op in group.ops:
+        if any(o.dtype not in _VEC4 for o in op.outs):
+            return 1
+    for x, r in ext:
+        xs = tuple(x.shape)
+        if r.dtype not in _VEC4:
+            return 1
+        if xs == shape or dtypes.element_count(xs) == 1:
+            continue
+        if len(xs) > len(shape) or any(a not in (1, b) for a, b in zip(xs[::-1], shape[::-1])):
+            return 1  # not a plain broadcast (e.g. a reshaped view): scalar path
+    return 4
+
+
+def _generate_group_x4(group: FusedGroup, ext, names, outs, idx_t):
+    """Fused elementwise kernel with 16-byte loads/stores (see _vector_width)."""
+    shape = tuple(group.shape)
+    lines = []
+    for k, (x, r) in enumerate(ext):
+        ct, vt = _CTYPE[r.dtype], _VEC4[r.dtype]
+        xs = tuple(x.shape)
+        if xs == shape:
+            lines.append(f"    const {vt} in{k}_v = ((const {vt}*)a.p[{k}])[t];")
+        elif dtypes.element_count(xs) == 1:
+            lines.append(f"    const {ct} in{k}_s = ((const {ct}*)a.p[{k}])[0];")
+            lines.append(f"    const {vt} in{k}_v = {{in{k}_s, in{k}_s, in{k}_s, in{k}_s}};")
+        else:
+            off = _index_expr(xs, shape, "i")
+            inner_bcast = len(xs) == 0 or xs[-1] == 1
+            if inner_bcast:
+                lines.append(f"    const {ct} in{k}_s = ((const {ct}*)a.p[{k}])[{off}];")
+                lines.append(f"    const {vt} in{k}_v = {{in{k}_s, in{k}_s, in{k}_s, in{k}_s}};")
+            else:
+                lines.append(f"    const {vt} in{k}_v = *(const {vt}*)((const {ct}*)a.p[{k}] + ({off}));")
+    body = []
+    for k, (x, r) in enumerate(ext):
+        body.append(f"      const {_CTYPE[r.dtype]} in{k} = ((const {_CTYPE[r.dtype]}*)&in{k}_v)[e];")
+
+    def ref(x: LV) -> str:
+        r = x.root()
+        nm = names.get((id(r), x.shape)) or names.get((id(r), r.shape))
+        if nm is not None:
+            return nm
+        if r.kind == "const" and r.imm is not None:
+            return c_literal(r.imm, r.dtype)
+        raise KernelError("fusion: unresolved operand")
+
+    for t, op in enumerate(group.ops):
+        o = op.outs[0]
+        ct = _CTYPE[o.dtype]
+        body.append(f"      const {ct} v{t} = {ew_expr(op.name, [ref(x) for x in op.ins], ct)};")
+        names[(id(o), o.shape)] = f"v{t}"
+    for k, o in enumerate(outs):
+        body.append(f"      ((({_CTYPE[o.dtype]}*)&out{k}_v))[e] = {names[(id(o), o.shape)]};")
+    decl = [f"    {_VEC4[o.dtype]} out{k}_v;" for k, o in enumerate(outs)]
+    stores = [f"    (({_VEC4[o.dtype]}*)a.p[{len(ext) + k}])[t] = out{k}_v;"
+              for k, o in enumerate(outs)]
+    n_ptr = len(ext) + len(outs)
+    src_core = (f"struct Params {{ void* p[{max(1, n_ptr)}]; long long n; }};\n"
+                f"extern \"C\" __global__ void __launch_bounds__(256) KNAME(const __grid_constant__ "
+                f"Params a) {{\n"
+                f"  const {idx_t} stride = ({idx_t})gridDim.x * blockDim.x;\n"
+                f"  const {idx_t} n4 = ({idx_t})(a.n >> 2);\n"
+                f"  for ({idx_t} t = ({idx_t})blockIdx.x * blockDim.x + threadIdx.x; t < n4;"
+                f" t += stride) {{\n"
+                f"    const {idx_t} i = t << 2;\n"
+                + "\n".join(lines + decl) + "\n"
+                f"#pragma unroll\n    for (int e = 0; e < 4; ++e) {{\n"
+                + "\n".join(body) + "\n    }\n"
+                + "\n".join(stores) + "\n  }\n}\n")
+    digest = hashlib.sha1(src_core.encode()).hexdigest()[:16]
+    name = f"sf_fused4_{digest}"
+    source = '#include "sf_ops.cuh"\n' + src_core.replace("KNAME", name)
+    return name, source, [r for _, r in ext], outs
+
+
 def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List[LV], List[LV]]:
     """CUDA source for a fused group. Returns (name, source, in_values, out_values)."""
     shape = group.shape
@@ -435,6 +542,10 @@ def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List
                 ext.append((x, r))
     outs = [op.outs[0] for op in group.ops if id(op.outs[0]) in needed_after]
     idx_t = "long long" if n >= (1 << 31) else "int"
+    vec = _vector_width(group, ext, outs)
+    group.vec = vec
+    if vec == 4:
+        return _generate_group_x4(group, ext, names, outs, idx_t)
     lines = []
     for k, (x, r) in enumerate(ext):
         ct = _CTYPE[r.dtype]

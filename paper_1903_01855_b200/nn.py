@@ -117,8 +117,31 @@ def _conv_grad(ctx):
     x, w = ctx.input(0), ctx.input(1)
     up = ctx.out_grad()
     a = {"stride": ctx.attrs["stride"], "pad": ctx.attrs["pad"]}
-    gx = dispatch("conv2d_grad_input", [up, w], dict(a, input_shape=tuple(ctx.in_spec(0)[1])))[0]
-    gw = dispatch("conv2d_grad_filter", [x, up], dict(a, filter_shape=tuple(ctx.in_spec(1)[1])))[0]
+    # one op for both gradients: the tf32 split of dy is made once and feeds
+    # the data-gradient and the filter-gradient GEMMs
+    gx, gw = dispatch("conv2d_grads", [x, w, up], a)
+    return [gx, gw]
+
+
+def _conv_grads_infer(attrs, in_specs, env=None):
+    return [in_specs[0], in_specs[1]]
+
+
+def _conv_grads_kernel(attrs, inputs, env):
+    x, w, dy = inputs
+    _check_float("conv2d_grads", x, w, dy)
+    n, h, wd, c = x.shape
+    kh, kw, ci, co = w.shape
+    dev = ordinal_of(env.device)
+    shared = None
+    if _use_tc(dy.dtype) and co % 4 == 0:
+        m = dy.shape[0] * dy.shape[1] * dy.shape[2]
+        shared = _native.split_tf32(dev, m, co, dy._ptr())  # (m, co): K-major A of the
+        # data gradient and MN-major B of the filter gradient
+    gi_attrs = {"stride": attrs["stride"], "pad": attrs["pad"], "input_shape": x.shape}
+    gf_attrs = {"stride": attrs["stride"], "pad": attrs["pad"], "filter_shape": w.shape}
+    gx = _conv_gi_kernel(gi_attrs, [dy, w], env, dy_split=shared)[0]
+    gw = _conv_gf_kernel(gf_attrs, [x, dy], env, dy_split=shared)[0]
     return [gx, gw]
 
 
@@ -126,7 +149,7 @@ def _conv_gi_infer(attrs, in_specs, env=None):
     return [(in_specs[0][0], tuple(attrs["input_shape"]))]
 
 
-def _conv_gi_kernel(attrs, inputs, env):
+def _conv_gi_kernel(attrs, inputs, env, dy_split=None):
     dy, w = inputs
     n, h, wd, c = attrs["input_shape"]
     kh, kw, ci, co = w.shape
@@ -135,7 +158,7 @@ def _conv_gi_kernel(attrs, inputs, env):
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
     if _use_tc(dy.dtype) and co % 4 == 0:
-        a = _native.split_tf32(dev, m, co, dy._ptr())      # dy, (m, co) K-major
+        a = dy_split or _native.split_tf32(dev, m, co, dy._ptr())  # dy, (m, co) K-major
         b = _native.split_tf32(dev, k, co, w._ptr())       # W as (k, co): B[n=k, k'=co]
         dcols = _tc(dev, m, k, co, a, b)                   # dy @ W^T
         del a, b
@@ -153,7 +176,7 @@ def _conv_gf_infer(attrs, in_specs, env=None):
     return [(in_specs[0][0], tuple(attrs["filter_shape"]))]
 
 
-def _conv_gf_kernel(attrs, inputs, env):
+def _conv_gf_kernel(attrs, inputs, env, dy_split=None):
     x, dy = inputs
     n, h, wd, c = x.shape
     kh, kw, ci, co = attrs["filter_shape"]
@@ -169,7 +192,7 @@ def _conv_gf_kernel(attrs, inputs, env):
             a = _native.split_tf32(dev, m, c, x._ptr())
         else:
             a = _native.im2col_split(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
-        b = _native.split_tf32(dev, m, co, dy._ptr())
+        b = dy_split or _native.split_tf32(dev, m, co, dy._ptr())
         dw = _native.gemm_tf32x3_ex(dev, kp, co, m, True, True, m, m, a[0].ptr, a[1].ptr,
                                     b[0].ptr, b[1].ptr)  # (kp, co); rows >= k unused
         del a, b
@@ -275,6 +298,7 @@ def nn_defs() -> List[OpDef]:
               _conv_gi_kernel, _conv_gi_infer),
         OpDef("conv2d_grad_filter", 2, _schema(stride=INT, pad=INT, filter_shape=SHAPE), 1,
               False, _conv_gf_kernel, _conv_gf_infer),
+        OpDef("conv2d_grads", 3, conv_attrs, 2, False, _conv_grads_kernel, _conv_grads_infer),
         OpDef("max_pool", 1, pool_attrs, 1, False, _pool_kernel, _pool_infer, _pool_grad),
         OpDef("max_pool_grad", 2, pool_attrs, 1, False, _pool_grad_kernel, _same_as_first),
         OpDef("softmax_xent", 2, {}, 1, False, _xent_kernel, _xent_infer, _xent_grad),

@@ -103,14 +103,35 @@ def test_int32_wraps():
     assert sf.reduce_sum(big).item() == int(np.sum(arr).astype(np.int32))
 
 
-@pytest.mark.parametrize("shape", [(100, 64), (20000, 3 * 64), (50000, 8), (33, 33)])
+@pytest.mark.parametrize("xs,ys", [((3136, 64), (64,)), ((3136, 64), (3136, 1)), ((50, 256), (1, 256)),
+                                   ((7, 2048), (7, 2048)), ((12, 4, 8), (4, 1)), ((6, 12), (12,))])
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div"])
+def test_row_column_broadcast_bitwise(xs, ys, op):
+    """2-D broadcasts (the vectorised NHWC-vs-channel path and its fallbacks)
+    are bit-exact with numpy's float32 arithmetic, in both operand orders."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(xs).astype(np.float32)
+    y = (rng.standard_normal(ys).astype(np.float32) + np.float32(3.0))
+    f = {"add": np.add, "sub": np.subtract, "mul": np.multiply, "div": np.divide}[op]
+    got = sf.dispatch(op, [sf.constant(x), sf.constant(y)])[0].numpy()
+    assert got.tobytes() == f(x, y).tobytes()
+    got = sf.dispatch(op, [sf.constant(y), sf.constant(x + np.float32(4.0))])[0].numpy()
+    assert got.tobytes() == f(y, x + np.float32(4.0)).tobytes()
+
+
+@pytest.mark.parametrize("shape", [(100, 64), (20000, 3 * 64), (50000, 8), (33, 33), (1568, 2048),
+                                   (3000, 256), (1025, 4), (40, 132), (301 * 1024 + 77, 64),
+                                   (600 * 1024, 128)])
 def test_column_reduction_matches_row_reduction_bitwise(shape):
-    """The coalesced column kernel and the warp kernel implement one order (CRO)."""
+    """The coalesced column kernels (scalar, and 16-byte at every block width)
+    and the warp kernel implement one order (CRO)."""
     rng = np.random.default_rng(9)
-    x = rng.standard_normal(shape).astype(np.float32)
+    x = rng.standard_normal(shape, dtype=np.float32)
+    x[:, 1] = -0.0  # an all-(-0.0) column sums to -0.0 (folds start from the first element)
     cols = sf.reduce_sum(sf.constant(x), axes=(0,)).numpy()
     rows = sf.reduce_sum(sf.constant(np.ascontiguousarray(x.T)), axes=(1,)).numpy()
     assert cols.tobytes() == rows.tobytes()
+    assert cols[1] == 0.0 and np.signbit(cols[1])
 
 
 def test_int32_mean_truncates_eagerly():
@@ -186,6 +207,29 @@ def test_single_op_eager_equals_staged():
         eager = sfops.dispatch(op, args, attrs)[0].numpy()
         staged = sf.stage(lambda *xs: sfops.dispatch(op, list(xs), attrs)[0])(*args).numpy()
         assert eager.tobytes() == staged.tobytes(), op
+
+
+@pytest.mark.parametrize("shape,bshape,cshape", [
+    ((16, 8, 64), (64,), (16, 8, 1)), ((256, 12), (1, 12), (256, 1)), ((4, 6, 6, 32), (32,), ()),
+    ((2, 512), (2, 512), (512,)), ((1023, 3), (3,), (1023, 1))])
+def test_fused_broadcast_groups_eager_equals_staged(shape, bshape, cshape):
+    """Fused elementwise groups (16-byte vector codegen when the innermost
+    extent allows it, scalar otherwise) are bit-exact with eager dispatch,
+    for row-, column- and scalar-broadcast operands and several outputs."""
+    rng = np.random.default_rng(11)
+    x = sf.constant(rng.standard_normal(shape).astype(np.float32))
+    b = sf.constant(rng.standard_normal(bshape).astype(np.float32))
+    c = sf.constant((rng.uniform(1.0, 2.0, cshape)).astype(np.float32))
+
+    def f(x, b, c):
+        y = sf.relu(x * b + c)
+        z = sf.exp(y / c) - x
+        return y, z * b
+
+    eager = f(x, b, c)
+    staged = sf.stage(f)(x, b, c)
+    for e, s in zip(eager, staged):
+        assert e.shape == s.shape and e.raw().tobytes() == s.raw().tobytes()
 
 
 @pytest.mark.parametrize("seed", range(50))
