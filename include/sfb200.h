@@ -68,6 +68,11 @@ int sf_alloc(int dev, size_t bytes, void** p);
 int sf_free(int dev, void* p);
 int sf_mem_stats(int dev, size_t* bytes_in_use, size_t* bytes_cached);
 int sf_trim(int dev);
+/* The device's arrival counters for single-launch multi-chunk column
+ * reductions (zero at rest; every kernel using them leaves them zero).
+ * Lowered (NVRTC) reduction kernels receive this address as a parameter.
+ * Replaces: nothing in the reference (np.sum is one call). */
+int sf_reduce_counters(int dev, void** counters);
 /* Page-locked host memory (cudaHostAlloc, portable).  Transfers to/from it
  * skip the staging copies: sf_memcpy_d2h writes it directly, sf_memcpy_h2d
  * reads it directly when the stream is idle. */

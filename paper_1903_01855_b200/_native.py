@@ -61,6 +61,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_mem_stats": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
                                          ctypes.POINTER(ctypes.c_size_t)]),
         "sf_trim": (ctypes.c_int, [ctypes.c_int]),
+        "sf_reduce_counters": (ctypes.c_int, [ctypes.c_int, _PVP]),
         "sf_host_alloc": (ctypes.c_int, [ctypes.c_size_t, _PVP]),
         "sf_host_free": (ctypes.c_int, [_VP]),
         "sf_memcpy_h2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
@@ -132,7 +133,7 @@ def _declare(lib: ctypes.CDLL) -> None:
 EXPORTED_SYMBOLS = (
     "sf_last_error", "sf_version", "sf_init", "sf_device_info", "sf_set_stream",
     "sf_get_stream", "sf_device_sync", "sf_alloc", "sf_free", "sf_mem_stats", "sf_trim",
-    "sf_host_alloc", "sf_host_free",
+    "sf_reduce_counters", "sf_host_alloc", "sf_host_free",
     "sf_memcpy_h2d", "sf_memcpy_d2h", "sf_memcpy_d2d", "sf_memcpy_p2p", "sf_elementwise",
     "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
@@ -428,6 +429,22 @@ def set_stream(dev: int, stream: int) -> None:
     rc = L.sf_set_stream(dev, stream or None)
     if rc:
         raise _err(L, rc, "sf_set_stream")
+
+
+_COUNTERS: dict = {}
+
+
+def reduce_counters(dev: int) -> int:
+    """Device address of the reduction arrival counters (fixed per process)."""
+    p = _COUNTERS.get(dev)
+    if p is None:
+        L = require_device()
+        out = ctypes.c_void_p(0)
+        rc = L.sf_reduce_counters(dev, ctypes.byref(out))
+        if rc:
+            raise _err(L, rc, "sf_reduce_counters")
+        p = _COUNTERS[dev] = out.value
+    return p
 
 
 def mem_stats(dev: int):

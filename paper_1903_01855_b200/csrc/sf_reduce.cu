@@ -10,6 +10,7 @@
 //   i32 sum wraps modulo 2^32 (numpy accumulates in int64, _wrap casts back).
 //   i32 mean (eager only; staged inference rejects it, kernels.py:344-352)
 //   accumulates in f64, divides, truncates to int32 like the astype in _wrap.
+#include <atomic>
 #include <type_traits>
 
 #include "sf_internal.h"
@@ -177,7 +178,9 @@ __global__ void __launch_bounds__(1024) reduce_cols(const T* __restrict__ in, lo
 // ... of the chunk, left to right, exactly the fold of reduce_cols — and the
 // 32 lane partials of each column are then combined by one warp with the xor
 // butterfly (the same tree; lanes past the chunk's end are absent).
-// XT column-quads per block; loads are issued in batches of 8 per thread.
+// XT column-quads per block; rows are staged in batches of 128 / XT.
+static constexpr int kColsStageBytes = 128 * 32 * 16;  // NB * XT * 32 float4 = 64 KB
+
 template <int XT>
 __global__ void __launch_bounds__(XT * 32) reduce_cols_f32x4(const float* __restrict__ in,
                                                              long long R, long long C,
@@ -187,7 +190,14 @@ __global__ void __launch_bounds__(XT * 32) reduce_cols_f32x4(const float* __rest
                                                              float countf,
                                                              unsigned* __restrict__ counters) {
   __shared__ float acc_s[32][XT * 4 + 1];
-  const int tx = threadIdx.x, tl = threadIdx.y;
+  // per-thread staging slots [NB][XT * 32] (dynamic, kColsStageBytes): a
+  // batch of NB rows is copied with cp.async, so all NB loads are in flight
+  // at once — with register loads ptxas interleaves load and add (the fold
+  // order is strict) and keeps only 2-3 loads outstanding, which starves
+  // HBM on the small grids of wide-channel layers
+  constexpr int NT = XT * 32, NB = 128 / XT;
+  extern __shared__ float4 stage[];
+  const int tx = threadIdx.x, tl = threadIdx.y, tid = tl * XT + tx;
   const long long c0 = ((long long)blockIdx.x * XT + tx) * 4;
   const long long j = blockIdx.y;
   const long long g0 = j * chunk;
@@ -198,38 +208,28 @@ __global__ void __launch_bounds__(XT * 32) reduce_cols_f32x4(const float* __rest
     const float* p = in + (g0 + tl) * C + c0;
     const long long step = 32 * C;
     const int n_rows = (int)((len - tl + 31) / 32);  // rows tl, tl+32, ... < len
-    int q = 0;
-    for (; q + 16 <= n_rows; q += 16) {
-      float4 v[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = *reinterpret_cast<const float4*>(p + (q + u) * step);
+    for (int q = 0; q < n_rows; q += NB) {
+      const int cnt = n_rows - q < NB ? n_rows - q : NB;
+      for (int u = 0; u < cnt; ++u) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&stage[u * NT + tid]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                     "l"(p + (q + u) * step)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
       // the lane's first element starts the fold (not 0 + x: keeps -0.0)
-      if (q == 0) acc = v[0];
-      else {
-        acc.x += v[0].x;
-        acc.y += v[0].y;
-        acc.z += v[0].z;
-        acc.w += v[0].w;
+      int u = 0;
+      if (q == 0) {
+        acc = stage[tid];
+        u = 1;
       }
-#pragma unroll
-      for (int u = 1; u < 16; ++u) {
-        acc.x += v[u].x;
-        acc.y += v[u].y;
-        acc.z += v[u].z;
-        acc.w += v[u].w;
+      for (; u < cnt; ++u) {
+        const float4 v = stage[u * NT + tid];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
       }
-    }
-    if (q == 0) {
-      acc = *reinterpret_cast<const float4*>(p);
-      q = 1;
-    }
-#pragma unroll 4
-    for (; q < n_rows; ++q) {
-      const float4 v = *reinterpret_cast<const float4*>(p + q * step);
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
     }
   }
   acc_s[tl][tx * 4 + 0] = acc.x;
@@ -300,9 +300,16 @@ __global__ void __launch_bounds__(XT * 32) reduce_cols_f32x4(const float* __rest
 template <int XT>
 static void launch_cols_x4(Device* d, const float* in, long long R, long long C, long long chunk,
                            long long n_chunks, float* part, float* out, int mean, float countf) {
+  static std::atomic<unsigned long long> attr_set{0};  // one bit per device
+  const unsigned long long bit = 1ull << (d->id & 63);
+  if (!(attr_set.load() & bit)) {
+    cudaFuncSetAttribute(reduce_cols_f32x4<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kColsStageBytes);
+    attr_set.fetch_or(bit);
+  }
   dim3 grid((unsigned)((C / 4 + XT - 1) / XT), (unsigned)n_chunks);
-  reduce_cols_f32x4<XT><<<grid, dim3(XT, 32), 0, d->stream>>>(in, R, C, chunk, n_chunks, part,
-                                                              out, mean, countf, d->red_counters);
+  reduce_cols_f32x4<XT><<<grid, dim3(XT, 32), kColsStageBytes, d->stream>>>(
+      in, R, C, chunk, n_chunks, part, out, mean, countf, d->red_counters);
 }
 
 // One launch: sum (or mean) over the rows of a row-major (R, C) float32

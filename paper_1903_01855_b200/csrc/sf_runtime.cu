@@ -313,6 +313,13 @@ int sf_free(int dev, void* p) {
   return d->alloc.release(p);
 }
 
+int sf_reduce_counters(int dev, void** counters) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  *counters = d->red_counters;
+  return SF_OK;
+}
+
 int sf_mem_stats(int dev, size_t* in_use, size_t* cached) {
   Device* d;
   SF_TRY(ensure_device(dev, &d));

@@ -25,7 +25,8 @@ from .errors import (CallbackError, DeadVariable, InputMismatch, KernelError, Mi
 from .graph import GraphFunction, Node
 from .kernels import KernelEnv, ordinal_of, relabel
 from .lowering import (FusedGroup, LOp, Lowerer, LV, PlanWriter, SLOT_CONST, SLOT_INPUT,
-                       SLOT_OUTPUT, SLOT_TEMP, cse, fuse, generate_group, pack_ew_step)
+                       SLOT_OUTPUT, SLOT_TEMP, cse, fuse, fuse_reductions, generate_group,
+                       generate_reduce_group, pack_ew_step)
 from .runtime import current_context, get_runtime
 from .tensor import Tensor
 
@@ -100,7 +101,7 @@ def _sm_count(dev: int) -> int:
 
 def _unit_ops(unit):
     if isinstance(unit, FusedGroup):
-        return unit.ops
+        return unit.ops + unit.reduces if unit.reduces else unit.ops
     if isinstance(unit, tuple):  # (RowProgram, planner)
         return unit[0].ops
     return [unit]
@@ -138,6 +139,8 @@ class Program:
         self.has_rng = any(op.kind in ("rng", "dropout") for op in ops)
         keep = frozenset(id(v.root()) for v in self.out_vals)
         units = fuse(plan_rows(ops, keep) if fuse_enabled else ops, fuse_enabled)
+        if fuse_enabled:
+            units = fuse_reductions(units)
         self.segments = self._segment(units)
         self.n_launches = sum(s.n_launches for s in self.segments
                               if isinstance(s, _NativeSegment))
@@ -264,7 +267,26 @@ class Program:
         seg.n_launches = n_launch
         return seg
 
+    def _emit_reduce_group(self, pw, group: FusedGroup, needed, use, define) -> int:
+        name, src, ext, outs, reds, grid, block, n_chunks, c = generate_reduce_group(
+            group, needed, _sm_count(self.dev))
+        kernel = _native.jit_compile(name, src)
+        in_slots = [use(r) for r in ext]
+        out_slots = [define(o) for o in outs]
+        red_slots = [define(op.outs[0]) for op in reds]
+        # chunk partials: scratch that lives for this launch only
+        part_slots = ([pw.slot(SLOT_TEMP, DType.float32, 4 * c * n_chunks) for _ in reds]
+                      if n_chunks > 1 else [])
+        ptrs = in_slots + out_slots + red_slots + part_slots
+        payload = struct.pack("<QIIII", kernel, grid, block, 0, len(ptrs))
+        payload += struct.pack("<%di" % len(ptrs), *ptrs)
+        payload += struct.pack("<IQ", 8, _native.reduce_counters(self.dev))
+        pw.step(1, payload, defs=out_slots + red_slots + part_slots, uses=in_slots)
+        return 1
+
     def _emit_group(self, pw, group: FusedGroup, needed, use, define) -> int:
+        if group.reduces:
+            return self._emit_reduce_group(pw, group, needed, use, define)
         if len(group.ops) == 1:
             return self._emit_single_ew(pw, group.ops[0], use, define)
         name, src, ext, outs = generate_group(group, needed)

@@ -262,7 +262,7 @@ def _splat_value(t: Tensor):
 
 
 class FusedGroup:
-    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs", "vec")
+    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs", "vec", "reduces")
 
     def __init__(self, shape):
         self.ops: List[LOp] = []
@@ -270,6 +270,7 @@ class FusedGroup:
         self.outs_needed: List[LV] = []
         self.ext_inputs: List[LV] = []
         self.vec = 1  # elements per thread of the generated kernel
+        self.reduces: List[LOp] = []  # column reductions folded in (fuse_reductions)
 
 
 _PURE_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "eye"))
@@ -458,8 +459,10 @@ def _vector_width(group: FusedGroup, ext, outs) -> int:
     return 4
 
 
-def _generate_group_x4(group: FusedGroup, ext, names, outs, idx_t):
-    """Fused elementwise kernel with 16-byte loads/stores (see _vector_width)."""
+def _x4_parts(group: FusedGroup, ext, names, outs, reds=()):
+    """Pieces of a 4-elements-per-thread group body over flat index i (t = i/4):
+    (operand loads, vector declarations, per-lane body, vector stores).  Each
+    value in ``reds`` (in-group LVs) is also exposed as float4 red{k}_v."""
     shape = tuple(group.shape)
     lines = []
     for k, (x, r) in enumerate(ext):
@@ -498,9 +501,18 @@ def _generate_group_x4(group: FusedGroup, ext, names, outs, idx_t):
         names[(id(o), o.shape)] = f"v{t}"
     for k, o in enumerate(outs):
         body.append(f"      ((({_CTYPE[o.dtype]}*)&out{k}_v))[e] = {names[(id(o), o.shape)]};")
+    for k, x in enumerate(reds):
+        body.append(f"      ((float*)&red{k}_v)[e] = {names[(id(x), x.shape)]};")
     decl = [f"    {_VEC4[o.dtype]} out{k}_v;" for k, o in enumerate(outs)]
+    decl += [f"    float4 red{k}_v;" for k in range(len(reds))]
     stores = [f"    (({_VEC4[o.dtype]}*)a.p[{len(ext) + k}])[t] = out{k}_v;"
               for k, o in enumerate(outs)]
+    return lines, decl, body, stores
+
+
+def _generate_group_x4(group: FusedGroup, ext, names, outs, idx_t):
+    """Fused elementwise kernel with 16-byte loads/stores (see _vector_width)."""
+    lines, decl, body, stores = _x4_parts(group, ext, names, outs)
     n_ptr = len(ext) + len(outs)
     src_core = (f"struct Params {{ void* p[{max(1, n_ptr)}]; long long n; }};\n"
                 f"extern \"C\" __global__ void __launch_bounds__(256) KNAME(const __grid_constant__ "
@@ -520,13 +532,11 @@ def _generate_group_x4(group: FusedGroup, ext, names, outs, idx_t):
     return name, source, [r for _, r in ext], outs
 
 
-def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List[LV], List[LV]]:
-    """CUDA source for a fused group. Returns (name, source, in_values, out_values)."""
-    shape = group.shape
-    n = dtypes.element_count(shape)
+def _group_ext(group: FusedGroup):
+    """External inputs of a group: [(view as consumed, storage root)] and the
+    name table; an alias (reshape) is loaded with its own shape over the
+    root's buffer."""
     produced = {id(o) for op in group.ops for o in op.outs}
-    # external inputs: (view as consumed, storage root); an alias (reshape)
-    # is loaded with its own shape over the root's buffer
     ext: List[Tuple[LV, LV]] = []
     names: Dict[Tuple[int, tuple], str] = {}
     for op in group.ops:
@@ -540,6 +550,193 @@ def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List
             if key not in names:
                 names[key] = f"in{len(ext)}"
                 ext.append((x, r))
+    return ext, names
+
+
+# ---------------------------------------------------------------------------
+# reduction fusion: column reductions folded into their producing group
+# ---------------------------------------------------------------------------
+
+RED_FUSE = True          # fold column reductions into the group computing their input
+_RED_MAX_PER_GROUP = 8
+
+
+def _column_geometry(x: LV):
+    """(R, C) when reducing x over all but its innermost axis is the float32
+    16-byte column kernel's case (reduce_cols_f32x4 in sf_reduce.cu), else None."""
+    shape = tuple(x.shape)
+    if x.dtype is not DType.float32 or len(shape) < 2 or None in shape:
+        return None
+    c = shape[-1]
+    r = dtypes.element_count(shape) // c if c else 0
+    if c % 4 or c < 8 or r <= 32 or c // 4 > 65536 or (r + 1023) // 1024 >= 65536:
+        return None
+    return r, c
+
+
+def fuse_reductions(units: List[Any]) -> List[Any]:
+    """Attach each column reduction (reduce_sum/mean over all but the last
+    axis) whose input is computed by an earlier fused group to that group:
+    the group's kernel then folds the value in registers instead of writing it
+    to HBM for a separate reduction launch.  The reduction moves to the
+    group's position, which is safe because its only input is computed there
+    and its consumers all come later.  The fold follows the eager kernel's
+    canonical order exactly, so results are unchanged bit for bit."""
+    if not RED_FUSE:
+        return units
+    out: List[Any] = []
+    where: Dict[int, int] = {}
+    for unit in units:
+        if isinstance(unit, FusedGroup):
+            for op in unit.ops:
+                where[id(op.outs[0])] = len(out)
+            out.append(unit)
+            continue
+        if (isinstance(unit, LOp) and unit.kind == "reduce"
+                and unit.name in ("reduce_sum", "reduce_mean")):
+            x = unit.ins[0]
+            g = where.get(id(x))
+            nd = len(x.shape)
+            if (g is not None and _column_geometry(x) is not None
+                    and tuple(sorted(unit.attrs.get("axes") or ())) == tuple(range(nd - 1))):
+                grp = out[g]
+                ext, _ = _group_ext(grp)
+                outs_all = [op.outs[0] for op in grp.ops]
+                if (tuple(grp.shape) == tuple(x.shape) and len(grp.reduces) < _RED_MAX_PER_GROUP
+                        and _vector_width(grp, ext, outs_all) == 4):
+                    grp.reduces.append(unit)
+                    continue
+        out.append(unit)
+    return out
+
+
+def generate_reduce_group(group: FusedGroup, needed_after: set, sm_count: int):
+    """CUDA source of a fused group that also folds column reductions of its
+    values (see fuse_reductions).  Thread (tx, l) of a block owns 4 adjacent
+    columns and partial lane l of one 1024-row chunk — rows l, l+32, ... —
+    computing the group's values there (storing the ones needed elsewhere) and
+    folding each reduced value left to right; the 32 lane partials of a column
+    are combined with the xor butterfly; with several chunks the last block of
+    a column group folds the chunk partials (arrival counter) and applies the
+    mean.  This is reduce_cols_f32x4 + reduce_partials' order exactly.
+
+    Returns (name, source, ext roots, stored outs, reduce ops, grid, block,
+    n_chunks, C)."""
+    shape = tuple(group.shape)
+    r_rows, c = _column_geometry(group.reduces[0].ins[0])
+    ext, names = _group_ext(group)
+    outs = [op.outs[0] for op in group.ops if id(op.outs[0]) in needed_after]
+    reds = group.reduces
+    k_red = len(reds)
+    chunk = min(1024, r_rows)
+    n_chunks = (r_rows + chunk - 1) // chunk
+    target = 4 * sm_count
+    xt = 32 if (c // 128) * n_chunks >= target else 16 if (c // 64) * n_chunks >= target else 8
+    while xt > 8 and k_red * 32 * (xt * 4 + 1) * 4 > 40000:
+        xt //= 2
+    gx = (c // 4 + xt - 1) // xt
+    lines, decl, body, stores = _x4_parts(group, ext, names, outs, [op.ins[0] for op in reds])
+    base_red = len(ext) + len(outs)
+    base_part = base_red + k_red
+    n_ptr = base_part + (k_red if n_chunks > 1 else 0)
+    fold = []
+    for k in range(k_red):
+        fold.append(f"      if (first) acc{k} = red{k}_v;\n      else {{ acc{k}.x += red{k}_v.x; "
+                    f"acc{k}.y += red{k}_v.y; acc{k}.z += red{k}_v.z; acc{k}.w += red{k}_v.w; }}")
+    countf = c_literal(float(r_rows), DType.float32)
+
+    def final(k, val):
+        o = f"((float*)a.p[{base_red + k}])[col]"
+        mean = reds[k].name == "reduce_mean"
+        return f"{o} = {val} / {countf};" if mean else f"{o} = {val};"
+
+    src = [f"struct Params {{ void* p[{n_ptr}]; unsigned* counters; }};",
+           f"extern \"C\" __global__ void __launch_bounds__({xt * 32}) KNAME("
+           f"const __grid_constant__ Params a) {{",
+           f"  __shared__ float acc_s[{k_red}][32][{xt * 4 + 1}];",
+           f"  const int tx = threadIdx.x % {xt}, tl = threadIdx.x / {xt};",
+           f"  const int bx = blockIdx.x % {gx};",
+           f"  const long long j = blockIdx.x / {gx};",
+           f"  const long long c0 = ((long long)bx * {xt} + tx) * 4;",
+           f"  const long long g0 = j * {chunk};",
+           f"  const long long len = {r_rows}LL - g0 < {chunk} ? {r_rows}LL - g0 : {chunk};"]
+    src += [f"  float4 acc{k} = make_float4(0.f, 0.f, 0.f, 0.f);" for k in range(k_red)]
+    src += [f"  if (c0 < {c} && tl < len) {{",
+            "    bool first = true;",
+            f"    for (long long row = g0 + tl; row < g0 + len; row += 32) {{",
+            f"    const long long i = row * {c} + c0;",
+            "    const long long t = i >> 2;"]
+    src += lines + decl
+    src += ["#pragma unroll", "    for (int e = 0; e < 4; ++e) {"] + body + ["    }"]
+    src += stores + fold + ["      first = false;", "    }", "  }"]
+    for k in range(k_red):
+        src += [f"  acc_s[{k}][tl][tx * 4 + 0] = acc{k}.x; acc_s[{k}][tl][tx * 4 + 1] = acc{k}.y;",
+                f"  acc_s[{k}][tl][tx * 4 + 2] = acc{k}.z; acc_s[{k}][tl][tx * 4 + 3] = acc{k}.w;"]
+    butterfly = ["#pragma unroll",
+                 "      for (int off = 16; off >= 1; off >>= 1) {",
+                 "        const float ov = __shfl_xor_sync(0xffffffffu, v, off);",
+                 "        const bool op = __shfl_xor_sync(0xffffffffu, present, off);",
+                 "        if (present && op) v = v + ov;",
+                 "        else if (op) v = ov;",
+                 "        present = present || op;",
+                 "      }"]
+    src += ["  __syncthreads();",
+            "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;",
+            f"  for (int k = 0; k < {k_red}; ++k) {{",
+            "#pragma unroll",
+            "    for (int q = 0; q < 4; ++q) {",
+            "      const int cl = warp * 4 + q;",
+            f"      const long long col = (long long)bx * {xt * 4} + cl;",
+            "      float v = acc_s[k][lane][cl];",
+            "      bool present = lane < len;"] + butterfly
+    if n_chunks == 1:
+        src += [f"      if (lane == 0 && col < {c}) {{",
+                "        switch (k) {"]
+        src += [f"          case {k}: {final(k, 'v')} break;" for k in range(k_red)]
+        src += ["        }", "      }", "    }", "  }", "}"]
+    else:
+        src += [f"      if (lane == 0 && col < {c}) "
+                f"((float*)a.p[{base_part} + k])[col * {n_chunks} + j] = v;",
+                "    }", "  }",
+                "  __shared__ bool last;",
+                "  __threadfence();",
+                "  __syncthreads();",
+                "  if (threadIdx.x == 0) {",
+                "    const unsigned prev = atomicAdd(&a.counters[bx], 1u);",
+                f"    last = prev == {n_chunks - 1}u;",
+                "    if (last) a.counters[bx] = 0;",
+                "  }",
+                "  __syncthreads();",
+                "  if (!last) return;",
+                "  __threadfence();",
+                f"  for (int k = 0; k < {k_red}; ++k) {{",
+                "    for (int q = 0; q < 4; ++q) {",
+                f"      const long long col = (long long)bx * {xt * 4} + warp * 4 + q;",
+                f"      if (col >= {c}) continue;",
+                f"      const float* pc = (const float*)a.p[{base_part} + k] + col * {n_chunks};",
+                "      float v = 0.f;",
+                "      bool present = false;",
+                f"      for (int qq = lane; qq < {n_chunks}; qq += 32) {{",
+                "        const float w = __ldcg(pc + qq);",
+                "        v = present ? v + w : w;",
+                "        present = true;",
+                "      }"] + butterfly
+        src += ["      if (lane == 0) {", "        switch (k) {"]
+        src += [f"          case {k}: {final(k, 'v')} break;" for k in range(k_red)]
+        src += ["        }", "      }", "    }", "  }", "}"]
+    src_core = "\n".join(src) + "\n"
+    digest = hashlib.sha1(src_core.encode()).hexdigest()[:16]
+    name = f"sf_fusedred_{digest}"
+    source = '#include "sf_ops.cuh"\n' + src_core.replace("KNAME", name)
+    return (name, source, [r for _, r in ext], outs, list(reds), gx * n_chunks, xt * 32,
+            n_chunks, c)
+
+
+def generate_group(group: FusedGroup, needed_after: set) -> Tuple[str, str, List[LV], List[LV]]:
+    """CUDA source for a fused group. Returns (name, source, in_values, out_values)."""
+    shape = group.shape
+    n = dtypes.element_count(shape)
+    ext, names = _group_ext(group)
     outs = [op.outs[0] for op in group.ops if id(op.outs[0]) in needed_after]
     idx_t = "long long" if n >= (1 << 31) else "int"
     vec = _vector_width(group, ext, outs)

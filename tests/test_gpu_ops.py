@@ -232,6 +232,36 @@ def test_fused_broadcast_groups_eager_equals_staged(shape, bshape, cshape):
         assert e.shape == s.shape and e.raw().tobytes() == s.raw().tobytes()
 
 
+@pytest.mark.parametrize("shape", [(2, 7, 7, 64), (32, 14, 14, 16), (4, 28, 28, 128), (3, 11, 13, 8),
+                                   (40, 1000)])
+def test_reduction_fusion_eager_equals_staged(shape):
+    """Normalisation-style graphs: column reductions folded into the group
+    that computes their input (one or several chunks, sum and mean, several
+    reductions per group, values also stored for later use) are bit-exact
+    with eager dispatch, which materialises every value and reduces it."""
+    from paper_1903_01855_b200 import lowering
+
+    rng = np.random.default_rng(13)
+    x = sf.constant(rng.standard_normal(shape).astype(np.float32))
+    g = sf.constant(rng.uniform(0.5, 1.5, shape[-1:]).astype(np.float32))
+    axes = tuple(range(len(shape) - 1))
+
+    def f(x, g):
+        mean = sf.reduce_mean(x, axes=axes)
+        xc = sf.sub(x, mean)
+        var = sf.reduce_mean(sf.mul(xc, xc), axes=axes)
+        y = sf.mul(sf.mul(xc, g), var)
+        s1 = sf.reduce_sum(sf.mul(y, x), axes=axes)
+        s2 = sf.reduce_sum(sf.relu(y), axes=axes, keepdims=True)
+        return y, var, s1, s2
+
+    eager = f(x, g)
+    assert lowering.RED_FUSE
+    staged = sf.stage(f)(x, g)
+    for e, s in zip(eager, staged):
+        assert e.shape == s.shape and e.raw().tobytes() == s.raw().tobytes()
+
+
 @pytest.mark.parametrize("seed", range(50))
 def test_random_programs_eager_equals_staged(seed):
     fn, inputs = random_pure_function(seed)
