@@ -157,6 +157,17 @@ def im2col_split(dev: int, geom: bytes, m: int, kp: int, src: int):
     return DeviceBuffer(dev, hi.value, m * kp * 4), DeviceBuffer(dev, lo.value, m * kp * 4)
 
 
+def im2col_raw(dev: int, geom: bytes, m: int, kp: int, src: int) -> DeviceBuffer:
+    """(m, kp) raw fp32 im2col rows, K zero-padded to kp (no lo part: for
+    GEMMs that derive it in shared memory)."""
+    L = require_device()
+    hi = ctypes.c_void_p(0)
+    rc = L.sf_im2col_split(dev, geom, kp, src, ctypes.byref(hi), None)
+    if rc:
+        raise _err(L, rc, "sf_im2col_split")
+    return DeviceBuffer(dev, hi.value, m * kp * 4)
+
+
 def gemm_tf32x3(dev: int, m: int, n: int, k: int, a_hi: int, a_lo: int, b_hi: int,
                 b_lo: int) -> "DeviceBuffer":
     """C[m,n] = A[m,k] . B[n,k]^T on tcgen05 (3xTF32); operands pre-split."""

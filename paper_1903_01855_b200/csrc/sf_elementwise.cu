@@ -102,19 +102,35 @@ __device__ __forceinline__ float4 fetch4(const EwArgs& a, int j, unsigned r, uns
   return *reinterpret_cast<const float4*>(p + r * s0 + c);
 }
 
+__device__ __forceinline__ float4 apply4(int op, float4 x, float4 y) {
+  float4 o;
+  o.x = apply<float, float>(op, x.x, y.x);
+  o.y = apply<float, float>(op, x.y, y.y);
+  o.z = apply<float, float>(op, x.z, y.z);
+  o.w = apply<float, float>(op, x.w, y.w);
+  return o;
+}
+
+// two independent vectors per thread and iteration (both loads in flight
+// before either result is needed)
 __global__ void __launch_bounds__(256) ew_2d_f32x4(const EwArgs a, float* __restrict__ out) {
   const unsigned n4 = (unsigned)(a.n >> 2), cols = (unsigned)a.shape[1];
   const unsigned stride = gridDim.x * blockDim.x;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+  const bool two = a.n_in > 1;
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + stride < n4; i += 2 * stride) {
+    const unsigned e0 = i << 2, r0 = e0 / cols, c0 = e0 - r0 * cols;
+    const unsigned e1 = (i + stride) << 2, r1 = e1 / cols, c1 = e1 - r1 * cols;
+    const float4 x0 = fetch4(a, 0, r0, c0), x1 = fetch4(a, 0, r1, c1);
+    const float4 y0 = two ? fetch4(a, 1, r0, c0) : x0, y1 = two ? fetch4(a, 1, r1, c1) : x1;
+    reinterpret_cast<float4*>(out)[i] = apply4(a.op, x0, y0);
+    reinterpret_cast<float4*>(out)[i + stride] = apply4(a.op, x1, y1);
+  }
+  for (; i < n4; i += stride) {
     const unsigned e = i << 2, r = e / cols, c = e - r * cols;
     const float4 x = fetch4(a, 0, r, c);
-    const float4 y = a.n_in > 1 ? fetch4(a, 1, r, c) : x;
-    float4 o;
-    o.x = apply<float, float>(a.op, x.x, y.x);
-    o.y = apply<float, float>(a.op, x.y, y.y);
-    o.z = apply<float, float>(a.op, x.z, y.z);
-    o.w = apply<float, float>(a.op, x.w, y.w);
-    reinterpret_cast<float4*>(out)[i] = o;
+    const float4 y = two ? fetch4(a, 1, r, c) : x;
+    reinterpret_cast<float4*>(out)[i] = apply4(a.op, x, y);
   }
 }
 

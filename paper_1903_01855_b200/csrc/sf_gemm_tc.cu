@@ -27,6 +27,11 @@
 namespace sfrt {
 
 static constexpr int TC_BM = 128, TC_BK = 32, TC_STAGES = 3;
+// smem ring depth: 64 KB stages (BN = 128) fit 3, 48 KB stages (BN = 64) fit 4
+template <int BN>
+struct TcStages {
+  static constexpr int n = BN <= 64 ? 4 : 3;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -111,6 +116,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// tf32 split of 4 values: *h = x with the low 13 mantissa bits cleared
+// (what the tensor core reads of x), returns lo = x - hi (exact in fp32)
+__device__ __forceinline__ float4 tf32_lo4(float4 v, float4* h) {
+  const unsigned m = 0xFFFFE000u;
+  h->x = __uint_as_float(__float_as_uint(v.x) & m);
+  h->y = __uint_as_float(__float_as_uint(v.y) & m);
+  h->z = __uint_as_float(__float_as_uint(v.z) & m);
+  h->w = __uint_as_float(__float_as_uint(v.w) & m);
+  return make_float4(v.x - h->x, v.y - h->y, v.z - h->z, v.w - h->w);
+}
+
 // Persistent variant: one CTA per SM walks the output tiles (and split-K
 // slices) round-robin.  Six warps:
 //   warp 0 lane 0: TMA producer over a TC_STAGES ring shared by all tiles
@@ -125,13 +141,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // e.g. A = cols^T of a weight-gradient GEMM read straight from cols): it is
 // loaded as 32x32 boxes and described with sw128_mn_desc, so no transposed
 // copy is ever made.
+// lo_a_smem / lo_b_smem: that operand's lo part is not read from HBM — the
+// four converter warps (6-9) derive it in shared memory from the TMA-loaded
+// fp32 tile (lo = x - tf32(x), elementwise, so the swizzled layout carries
+// over unchanged), halving the operand bytes the TMA moves per k-block and
+// making the separate split pass unnecessary.  The MMA issuer then waits on
+// the converters' barrier instead of the TMA's.
 template <int BN, bool AMN, bool BMN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap tAhi,
                        const __grid_constant__ CUtensorMap tAlo,
                        const __grid_constant__ CUtensorMap tBhi,
                        const __grid_constant__ CUtensorMap tBlo, float* __restrict__ C, int M,
-                       int N, int K, int kb_per_split, int tiles_n, int tiles_mn, int n_tiles) {
+                       int N, int K, int kb_per_split, int tiles_n, int tiles_mn, int n_tiles,
+                       int lo_a_smem, int lo_b_smem) {
+  constexpr int TC_STAGES = TcStages<BN>::n;  // shadows the default ring depth
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4, B_BYTES = BN * TC_BK * 4;
   constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -140,13 +164,16 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + TC_STAGES;
   uint64_t* acc_full = empty + TC_STAGES;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+  uint64_t* conv = acc_empty + 2;
+  uint32_t* tmem_slot = (uint32_t*)(conv + TC_STAGES);
+  const bool any_lo = lo_a_smem || lo_b_smem;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -179,28 +206,31 @@ __global__ void __launch_bounds__(192, 1)
           const int s = g % TC_STAGES;
           if (g >= TC_STAGES) mbar_wait(&empty[s], ((g / TC_STAGES) & 1u) ^ 1u);
           uint8_t* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], STAGE_BYTES);
+          mbar_expect_tx(&full[s], (lo_a_smem ? A_BYTES : 2 * A_BYTES) +
+                                       (lo_b_smem ? B_BYTES : 2 * B_BYTES));
           const int kx = kb * TC_BK;
           if constexpr (AMN) {
 #pragma unroll
             for (int j = 0; j < TC_BM / 32; ++j) {
               tma_load_2d(st + 4096 * j, &tAhi, &full[s], m0 + 32 * j, kx);
-              tma_load_2d(st + A_BYTES + 4096 * j, &tAlo, &full[s], m0 + 32 * j, kx);
+              if (!lo_a_smem)
+                tma_load_2d(st + A_BYTES + 4096 * j, &tAlo, &full[s], m0 + 32 * j, kx);
             }
           } else {
             tma_load_2d(st, &tAhi, &full[s], kx, m0);
-            tma_load_2d(st + A_BYTES, &tAlo, &full[s], kx, m0);
+            if (!lo_a_smem) tma_load_2d(st + A_BYTES, &tAlo, &full[s], kx, m0);
           }
           if constexpr (BMN) {
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j) {
               tma_load_2d(st + 2 * A_BYTES + 4096 * j, &tBhi, &full[s], n0 + 32 * j, kx);
-              tma_load_2d(st + 2 * A_BYTES + B_BYTES + 4096 * j, &tBlo, &full[s], n0 + 32 * j,
-                          kx);
+              if (!lo_b_smem)
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES + 4096 * j, &tBlo, &full[s],
+                            n0 + 32 * j, kx);
             }
           } else {
             tma_load_2d(st + 2 * A_BYTES, &tBhi, &full[s], kx, n0);
-            tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
+            if (!lo_b_smem) tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
           }
         }
       }
@@ -231,6 +261,13 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t pb[3] = {b_hi, b_lo, b_hi};
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
+            if (pass == 1 && any_lo) {
+              // hi.hi needs only the TMA'd tiles and is already issued; the
+              // passes reading lo wait for the converters (their work hides
+              // behind the tensor core's pass 0)
+              mbar_wait(&conv[s], (g / TC_STAGES) & 1u);
+              asm volatile("tcgen05.fence::after_thread_sync;");
+            }
 #pragma unroll
             for (int j = 0; j < TC_BK / 8; ++j) {
               const uint64_t da = AMN ? sw128_mn_desc(pa[pass] + 1024u * j)
@@ -243,6 +280,44 @@ __global__ void __launch_bounds__(192, 1)
           mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[b]);
+      }
+    }
+  } else if (warp >= 6) {
+    // converter warps 6..9: lo parts of the stage's tiles, in ring order
+    if (any_lo) {
+      const int ct = threadIdx.x - 192;  // 0..127
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int z = t / tiles_mn;
+        const int kb0 = z * kb_per_split;
+        const int kb1 = kb0 + kb_per_split < nk_all ? kb0 + kb_per_split : nk_all;
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % TC_STAGES;
+          mbar_wait(&full[s], (g / TC_STAGES) & 1u);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          if (lo_a_smem) {
+            const float4* hi = reinterpret_cast<const float4*>(st);
+            float4* lo = reinterpret_cast<float4*>(st + A_BYTES);
+#pragma unroll
+            for (int i = 0; i < (int)(A_BYTES / 16 / 128); ++i) {
+              float4 h;
+              lo[ct + 128 * i] = tf32_lo4(hi[ct + 128 * i], &h);
+            }
+          }
+          if (lo_b_smem) {
+            const float4* hi = reinterpret_cast<const float4*>(st + 2 * A_BYTES);
+            float4* lo = reinterpret_cast<float4*>(st + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+            for (int i = 0; i < (int)(B_BYTES / 16 / 128); ++i) {
+              float4 h;
+              lo[ct + 128 * i] = tf32_lo4(hi[ct + 128 * i], &h);
+            }
+          }
+          // generic-proxy smem writes -> visible to the tensor core (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);
+        }
       }
     }
   } else {
@@ -325,15 +400,6 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict
 
 // Same split with 16-byte accesses, two vectors in flight per thread and
 // iteration (HBM-bound: 4 B read + 4 B written per element when hi is skipped).
-__device__ __forceinline__ float4 tf32_lo4(float4 v, float4* h) {
-  const unsigned m = 0xFFFFE000u;
-  h->x = __uint_as_float(__float_as_uint(v.x) & m);
-  h->y = __uint_as_float(__float_as_uint(v.y) & m);
-  h->z = __uint_as_float(__float_as_uint(v.z) & m);
-  h->w = __uint_as_float(__float_as_uint(v.w) & m);
-  return make_float4(v.x - h->x, v.y - h->y, v.z - h->z, v.w - h->w);
-}
-
 __global__ void __launch_bounds__(256) split_tf32_x4_kernel(const float* __restrict__ x,
                                                             float* __restrict__ hi,
                                                             float* __restrict__ lo, long long n) {
@@ -418,6 +484,10 @@ template <int BN, bool AMN, bool BMN>
 static int run_tc(Device* d, long long M, long long N, long long K, long long ak, long long bk,
                   const float* ahi, const float* alo, const float* bhi, const float* blo,
                   float* c) {
+  // a null lo pointer: that operand's lo part is derived in shared memory
+  const int lo_a_smem = alo == nullptr, lo_b_smem = blo == nullptr;
+  if (lo_a_smem) alo = ahi;  // the (unused) lo map still needs a valid encoding
+  if (lo_b_smem) blo = bhi;
   CUtensorMap ta, tal, tb, tbl;
   if (AMN) {
     SF_TRY(encode_map(&ta, ahi, ak, M, 32, true));
@@ -433,7 +503,7 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
     SF_TRY(encode_map(&tb, bhi, N, bk, BN));
     SF_TRY(encode_map(&tbl, blo, N, bk, BN));
   }
-  const int smem = TC_STAGES * (2 * TC_BM * TC_BK * 4 + 2 * BN * TC_BK * 4) + 1024 + 256;
+  const int smem = TcStages<BN>::n * (2 * TC_BM * TC_BK * 4 + 2 * BN * TC_BK * 4) + 1024 + 256;
   static bool configured[64] = {};
   if (!configured[d->id]) {
     SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN, AMN, BMN>,
@@ -459,9 +529,9 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
   if (splits > 1)
     SF_TRY(d->alloc.alloc(d->id, sizeof(float) * (size_t)(splits * M * N), (void**)&work));
   if (work) out = work;
-  gemm_tc_persistent<BN, AMN, BMN><<<grid, 192, smem, d->stream>>>(
+  gemm_tc_persistent<BN, AMN, BMN><<<grid, 320, smem, d->stream>>>(
       ta, tal, tb, tbl, out, (int)M, (int)N, (int)K, (int)per, (int)tiles_n, (int)tiles,
-      (int)n_tiles);
+      (int)n_tiles, lo_a_smem, lo_b_smem);
   if (splits == 1) {
     count_launch(d->id);
     SF_CHECK_CUDA(cudaGetLastError());

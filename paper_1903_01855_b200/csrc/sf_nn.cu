@@ -179,6 +179,10 @@ __global__ void im2col_split_kernel(const float* __restrict__ x, float* __restri
       const long long ih = oh * g.s - g.p + kh, iw = ow * g.s - g.p + kw;
       if (ih >= 0 && ih < g.h && iw >= 0 && iw < g.w) v = x[((n * g.h + ih) * g.w + iw) * g.c + c];
     }
+    if (lo == nullptr) {  // raw padded cols (the GEMM derives lo in shared memory)
+      hi[i] = v;
+      continue;
+    }
     const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     hi[i] = h;
     lo[i] = v - h;
@@ -492,16 +496,22 @@ int sf_im2col_split(int dev, const int64_t* g8, int64_t kp, const void* x, void*
   const ConvGeom g = geom(g8);
   const long long total = g.n * g.ho * g.wo * kp;
   if (*hi == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * 4, hi));
-  if (*lo == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * 4, lo));
+  // lo == NULL: raw fp32 cols, K padded to kp, no lo part (for GEMMs that
+  // derive lo in shared memory)
+  if (lo && *lo == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)total * 4, lo));
   if (total == 0) return SF_OK;
   count_launch(dev);
   if (seg_ok(g, kp, 4)) {
     const long long segs = g.n * g.ho * g.wo * (g.kh * g.kw + 1);
-    im2col_seg_kernel<float, true><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
-        (const float*)x, (float*)*hi, (float*)*lo, g, (int)kp);
+    if (lo)
+      im2col_seg_kernel<float, true><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
+          (const float*)x, (float*)*hi, (float*)*lo, g, (int)kp);
+    else
+      im2col_seg_kernel<float, false><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
+          (const float*)x, (float*)*hi, nullptr, g, (int)kp);
   } else {
     im2col_split_kernel<<<grid_for_n(d, total), 256, 0, d->stream>>>(
-        (const float*)x, (float*)*hi, (float*)*lo, g, kp);
+        (const float*)x, (float*)*hi, lo ? (float*)*lo : nullptr, g, kp);
   }
   SF_CHECK_CUDA(cudaGetLastError());
   return SF_OK;

@@ -45,10 +45,34 @@ def _ceil4(v: int) -> int:
     return (v + 3) // 4 * 4
 
 
+# GEMM operands stay raw fp32 in HBM; the GEMM kernel derives each tf32 lo
+# part in shared memory from the tile it loaded (sf_gemm_tc.cu converter
+# warps).  False: lo parts are precomputed by a separate split pass.
+LO_IN_SMEM = True
+
+
+def _lo(pair) -> int:
+    return pair[1].ptr if pair[1] is not None else 0
+
+
+def _raw(dev, rows, cols, ptr):
+    """(hi, lo) operand pair for a K-major fp32 matrix at ptr."""
+    if LO_IN_SMEM:
+        return (_native.RawRef(ptr), None)
+    return _native.split_tf32(dev, rows, cols, ptr)
+
+
+def _cols(dev, geom, m, kp, ptr):
+    """(hi, lo) operand pair of the K-padded im2col rows of the input at ptr."""
+    if LO_IN_SMEM:
+        return (_native.im2col_raw(dev, geom, m, kp, ptr), None)
+    return _native.im2col_split(dev, geom, m, kp, ptr)
+
+
 def _tc(dev, m, n, k, a_hilo, b_hilo):
     """C[m,n] = A[m,k] . B[n,k]^T on tcgen05 (3xTF32); a/b given as (hi, lo)."""
-    return _native.gemm_tf32x3(dev, m, n, k, a_hilo[0].ptr, a_hilo[1].ptr, b_hilo[0].ptr,
-                               b_hilo[1].ptr)
+    return _native.gemm_tf32x3(dev, m, n, k, a_hilo[0].ptr, _lo(a_hilo), b_hilo[0].ptr,
+                               _lo(b_hilo))
 
 
 def _use_tc(dt: DType) -> bool:
@@ -91,14 +115,14 @@ def _conv_kernel(attrs, inputs, env):
     if _use_tc(x.dtype):
         kp = _ceil4(k)
         if _is_pointwise(kh, kw, s, p) and kp == k:
-            a = _native.split_tf32(dev, m, k, x._ptr())  # x itself is the hi operand
+            a = _raw(dev, m, k, x._ptr())  # x itself is the A operand
         else:
-            a = _native.im2col_split(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
+            a = _cols(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
         if co % 4 == 0:
             # W (k, co) read MN-major: no transposed copy; rows >= k read as 0
-            b = _native.split_tf32(dev, k, co, w._ptr())
-            out = _native.gemm_tf32x3_ex(dev, m, co, kp, False, True, kp, k, a[0].ptr, a[1].ptr,
-                                         b[0].ptr, b[1].ptr)
+            b = _raw(dev, k, co, w._ptr())
+            out = _native.gemm_tf32x3_ex(dev, m, co, kp, False, True, kp, k, a[0].ptr, _lo(a),
+                                         b[0].ptr, _lo(b))
         else:
             b = _native.split_tf32(dev, k, co, w._ptr(), transpose=True, ldo=kp)  # W^T
             out = _tc(dev, m, co, kp, a, b)
@@ -136,8 +160,8 @@ def _conv_grads_kernel(attrs, inputs, env):
     shared = None
     if _use_tc(dy.dtype) and co % 4 == 0:
         m = dy.shape[0] * dy.shape[1] * dy.shape[2]
-        shared = _native.split_tf32(dev, m, co, dy._ptr())  # (m, co): K-major A of the
-        # data gradient and MN-major B of the filter gradient
+        shared = _raw(dev, m, co, dy._ptr())  # (m, co): K-major A of the data
+        # gradient and MN-major B of the filter gradient
     gi_attrs = {"stride": attrs["stride"], "pad": attrs["pad"], "input_shape": x.shape}
     gf_attrs = {"stride": attrs["stride"], "pad": attrs["pad"], "filter_shape": w.shape}
     gx = _conv_gi_kernel(gi_attrs, [dy, w], env, dy_split=shared)[0]
@@ -158,8 +182,8 @@ def _conv_gi_kernel(attrs, inputs, env, dy_split=None):
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
     if _use_tc(dy.dtype) and co % 4 == 0:
-        a = dy_split or _native.split_tf32(dev, m, co, dy._ptr())  # dy, (m, co) K-major
-        b = _native.split_tf32(dev, k, co, w._ptr())       # W as (k, co): B[n=k, k'=co]
+        a = dy_split or _raw(dev, m, co, dy._ptr())   # dy, (m, co) K-major
+        b = _raw(dev, k, co, w._ptr())                # W as (k, co): B[n=k, k'=co]
         dcols = _tc(dev, m, k, co, a, b)                   # dy @ W^T
         del a, b
     else:
@@ -189,12 +213,12 @@ def _conv_gf_kernel(attrs, inputs, env, dy_split=None):
         # cols (m, kp) and dy (m, co): no transposed copies
         kp = _ceil4(k)
         if _is_pointwise(kh, kw, s, p):
-            a = _native.split_tf32(dev, m, c, x._ptr())
+            a = _raw(dev, m, c, x._ptr())
         else:
-            a = _native.im2col_split(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
-        b = dy_split or _native.split_tf32(dev, m, co, dy._ptr())
-        dw = _native.gemm_tf32x3_ex(dev, kp, co, m, True, True, m, m, a[0].ptr, a[1].ptr,
-                                    b[0].ptr, b[1].ptr)  # (kp, co); rows >= k unused
+            a = _cols(dev, _geom(n, h, wd, c, kh, kw, s, p), m, kp, x._ptr())
+        b = dy_split or _raw(dev, m, co, dy._ptr())
+        dw = _native.gemm_tf32x3_ex(dev, kp, co, m, True, True, m, m, a[0].ptr, _lo(a),
+                                    b[0].ptr, _lo(b))  # (kp, co); rows >= k unused
         del a, b
     elif _use_tc(x.dtype):
         mp = _ceil4(m)

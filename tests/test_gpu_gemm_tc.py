@@ -86,3 +86,28 @@ def test_gemm_mn_major_operands(a_mn, b_mn, m, n, k, ak, bk):
         bh2, bl2 = _native.split_tf32(0, n, k, tb2._ptr())
         ref = _native.gemm_tf32x3(0, m, n, k, ah2.ptr, al2.ptr, bh2.ptr, bl2.ptr)
         assert _native.download(ref, np.float32, (m, n)).tobytes() == got.tobytes()
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("lo_a,lo_b", [(True, True), (True, False), (False, True)])
+@pytest.mark.parametrize("m,n,k,ak,bk", [(128, 64, 64, 64, 64), (200, 96, 100, 100, 97),
+                                         (516, 256, 3000, 3000, 3000), (1000, 200, 36, 36, 33)])
+def test_gemm_lo_in_shared_memory_bitwise(a_mn, b_mn, lo_a, lo_b, m, n, k, ak, bk):
+    """A NULL lo pointer makes the GEMM derive that operand's tf32 lo part in
+    shared memory from the raw fp32 tile (converter warps) instead of reading
+    a precomputed lo matrix: same lo values, same MMA sequence, same bits."""
+    if (not a_mn and ak % 4) or (not b_mn and bk % 4):
+        pytest.skip("K-major leading dimension must be a multiple of 4")
+    rng = np.random.default_rng(m + 3 * n + k)
+    a = rng.standard_normal((m, ak)).astype(np.float32)
+    b = rng.standard_normal((n, bk)).astype(np.float32)
+    a_store = np.ascontiguousarray(a.T if a_mn else a)
+    b_store = np.ascontiguousarray(b.T if b_mn else b)
+    ta, tb = sf.constant(a_store), sf.constant(b_store)
+    ah, al = _native.split_tf32(0, *a_store.shape, ta._ptr())
+    bh, bl = _native.split_tf32(0, *b_store.shape, tb._ptr())
+    ref = _native.gemm_tf32x3_ex(0, m, n, k, a_mn, b_mn, ak, bk, ah.ptr, al.ptr, bh.ptr, bl.ptr)
+    got = _native.gemm_tf32x3_ex(0, m, n, k, a_mn, b_mn, ak, bk, ta._ptr(),
+                                 0 if lo_a else al.ptr, tb._ptr(), 0 if lo_b else bl.ptr)
+    r = _native.download(ref, np.float32, (m, n))
+    assert _native.download(got, np.float32, (m, n)).tobytes() == r.tobytes()
