@@ -468,6 +468,10 @@ def extras(sf, np, _native, plugins, l2hmc):
     c2["staged_over_eager"] = c2["staged"]["ops_per_sec"] / c2["eager"]["ops_per_sec"]
     out["c2_microbench"] = c2
     out["c4_resnet50_b32"] = resnet_extra(sf, np, _native)
+    try:
+        out["c5_resnet50_b256_1gpu"] = c5_extra(sf, _native, 0, 1, None)
+    except Exception as e:  # report, never lose the headline line
+        out["c5_resnet50_b256_1gpu"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     out["f1_device_while"] = while_extra(sf, np, _native)
     return out
 
@@ -512,9 +516,11 @@ def while_extra(sf, np, _native):
     return row
 
 
-def c5_extra(sf, _native, rank, world, dist):
-    """C5: ResNet-50 data parallel, batch 32 per GPU, bucketed NCCL gradient
-    all-reduce on the backend stream; device time per step, max over ranks."""
+def c5_extra(sf, _native, rank, world, dist, batch=256):
+    """C5: ResNet-50 data parallel, batch 256 per GPU (BASELINE config 5),
+    bucketed NCCL gradient all-reduce on the backend stream; device time per
+    step, max over ranks.  At world 1 there is no collective (the per-GPU
+    compute of the same step)."""
     import torch
 
     from paper_1903_01855_b200 import dist as sfdist
@@ -523,11 +529,12 @@ def c5_extra(sf, _native, rank, world, dist):
     sf.init_runtime(sf.RuntimeOptions())
     nn.install()
     stream = sfdist.run_on_backend_stream(0)
-    dp = sfdist.ResNetDataParallel(sf, batch_per_rank=32, rank=rank, world=world)
+    dp = sfdist.ResNetDataParallel(sf, batch_per_rank=batch, rank=rank, world=world)
     for _ in range(3):
         dp.step()
     _native.sync(0)
-    dist.barrier()
+    if dist is not None:
+        dist.barrier()
     n = 5
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -535,13 +542,20 @@ def c5_extra(sf, _native, rank, world, dist):
         dp.step()
     e1.record(stream)
     _native.sync(0)
-    t = torch.tensor([e0.elapsed_time(e1) / n], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = e0.elapsed_time(e1) / n
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     torch.cuda.set_stream(torch.cuda.default_stream(0))
-    return {"img_per_sec": 32 * world / (ms / 1e3), "ms_per_step": ms, "batch_per_gpu": 32,
-            "buckets": len(dp.reducer.buckets), "scaling": "weak",
-            "collective": "NCCL all_reduce(sum) of 25 MiB flat fp32 buckets, lr/N update"}
+    out = {"img_per_sec": batch * world / (ms / 1e3), "ms_per_step": ms, "batch_per_gpu": batch,
+           "n_gpus": world, "scaling": "weak"}
+    if dist is not None:
+        out.update(buckets=len(dp.reducer.buckets),
+                   collective="NCCL all_reduce(sum) of 25 MiB flat fp32 buckets, lr/N update")
+    else:
+        out["collective"] = "none (one GPU: the per-GPU compute of the DP step)"
+    return out
 
 
 def resnet_extra(sf, np, _native):

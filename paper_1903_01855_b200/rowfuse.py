@@ -322,10 +322,46 @@ def _split(rp: RowProgram, planner) -> List[RowProgram]:
 ROW, UNI, BAD = "row", "uni", "bad"
 
 
+def variable_derived(ops: List[LOp]) -> set:
+    """ids of chain-independent values: variables, the weight operands of
+    matmuls (the B side, traced back to the graph inputs they come from), and
+    everything computed from those and constants only.  Such a value stays
+    uniform even when its leading extent happens to equal the batch (10
+    chains through 10-wide layers: W is (10, 10) and W_out (10, 2) looks like
+    the chain state), so the planner does not mistake it for rows."""
+    prod: Dict[int, LOp] = {}
+    for op in ops:
+        for o in getattr(op, "outs", ()):
+            prod[id(o)] = op
+    vd: set = set()
+    stack = [op.ins[1].root() for op in ops
+             if getattr(op, "kind", None) == "matmul" and not op.attrs.get("tb")]
+    while stack:
+        r = stack.pop()
+        if id(r) in vd:
+            continue
+        vd.add(id(r))
+        p = prod.get(id(r))
+        if p is not None and p.kind in ("ew", "transpose", "matmul", "var_read"):
+            stack.extend(x.root() for x in p.ins)
+    for op in ops:
+        if isinstance(op, tuple) or not getattr(op, "ins", None):
+            continue
+        if op.kind == "var_read":
+            vd.update(id(o) for o in op.outs)
+            continue
+        srcs = [x.root() for x in op.ins]
+        if any(id(r) in vd or r.kind == "var" for r in srcs) and all(
+                id(r) in vd or r.kind in ("var", "const") for r in srcs):
+            vd.update(id(o) for o in op.outs)
+    return vd
+
+
 class RowPlanner:
-    def __init__(self, batch: int):
+    def __init__(self, batch: int, uniform_ids=frozenset()):
         self.B = batch
         self.layout: Dict[int, Tuple] = {}
+        self.uniform_ids = uniform_ids  # variable-derived values (see variable_derived)
 
     def layout_of(self, lv: LV) -> Tuple:
         L = self.layout.get(id(lv))
@@ -341,6 +377,8 @@ class RowPlanner:
                     L = (BAD,)
             else:
                 L = (BAD,)
+        elif id(lv) in self.uniform_ids or lv.kind == "var":
+            L = (UNI,)
         else:
             L = self._shape_layout(lv.shape)
         self.layout[id(lv)] = L
@@ -435,7 +473,7 @@ def plan_rows(ops: List[LOp], keep=frozenset()) -> List:
             users.setdefault(id(x.root()), []).append(op)
     # no batch dimension (e.g. the C2 chain on (1, 16)): every value is uniform
     # and runs of small ops become one-warp uniform kernels
-    planner = RowPlanner(batch if batch >= MIN_BATCH else -1)
+    planner = RowPlanner(batch if batch >= MIN_BATCH else -1, variable_derived(ops))
     units: List = []
     cur: Optional[RowProgram] = None
     for op in ops:

@@ -67,8 +67,10 @@ def test_l2hmc_matches_reference_golden_host_rng(b):
         np.testing.assert_allclose(got, GOLD[f"l2hmc_{mode}_{b}"], rtol=RTOL, atol=1e-5)
 
 
-@pytest.mark.parametrize("b", [200, 5000])
+@pytest.mark.parametrize("b", [2, 10, 200, 5000])
 def test_l2hmc_eager_equals_staged_device_rng(b):
+    # b = 2 and 10 equal the sampler's layer widths: weights then have the
+    # batch's leading extent and must still be planned as uniform operands
     outs = {}
     for mode in ("eager", "staged"):
         sf.init_runtime(sf.RuntimeOptions(seed=3))

@@ -79,6 +79,25 @@ def test_reroll_refuses_when_an_intermediate_step_escapes():
         assert all(id(v) not in body_outs for v in P.ops[7].outs)
 
 
+def test_batch_equal_to_layer_width_keeps_weights_uniform():
+    """4 chains through 4-wide layers: the (4, 4) weights read from variables
+    have the batch's leading extent but are chain-independent — they must be
+    uniform operands of one row program, not rows."""
+    P = _Prog()
+    x = P.lv((4, 4), "input")
+    wv = P.lv((4, 4), "var")
+    w = P.op("var_read", "var_read", [wv], (4, 4))
+    wt = P.op("ew", "mul", [w, w], (4, 4))  # a weight transform: still uniform
+    h = P.op("matmul", "matmul", [x, wt], (4, 4))
+    y = P.op("ew", "tanh", [h], (4, 4))
+    assert rowfuse.choose_batch(P.ops) == 4
+    units = rowfuse.plan_rows(P.ops, {id(y)})
+    rows = [u for u in units if isinstance(u, tuple) and not u[0].uniform_only]
+    assert len(rows) == 1
+    names = [op.name for op in rows[0][0].ops]
+    assert "matmul" in names and "tanh" in names
+
+
 def test_rerolled_program_generates_and_compiles():
     P, keep, out = _steps(6)
     units = rowfuse.plan_rows(P.ops, keep)
