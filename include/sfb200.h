@@ -83,6 +83,12 @@ int sf_host_free(void* p);
  * caller may reuse `src` immediately); d2h blocks until the data is on the
  * host. */
 int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes);
+/* h2d from a source the caller guarantees immutable and alive until the
+ * copy has executed (a read-only host array the new tensor keeps): a
+ * page-locked source is DMA'd without waiting (*async = 1), others take the
+ * sf_memcpy_h2d path.  Replaces: tensor_from_host's copy,
+ * stageflow/tensor.py:138-162. */
+int sf_memcpy_h2d_immutable(int dev, void* dst, const void* src, size_t bytes, int* async);
 int sf_memcpy_d2h(int dev, void* dst, const void* src, size_t bytes);
 int sf_memcpy_d2d(int dev, void* dst, const void* src, size_t bytes);
 int sf_memcpy_p2p(int dst_dev, void* dst, int src_dev, const void* src, size_t bytes);

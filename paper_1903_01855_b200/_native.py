@@ -65,6 +65,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_host_alloc": (ctypes.c_int, [ctypes.c_size_t, _PVP]),
         "sf_host_free": (ctypes.c_int, [_VP]),
         "sf_memcpy_h2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
+        "sf_memcpy_h2d_immutable": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t,
+                                                   ctypes.POINTER(ctypes.c_int)]),
         "sf_memcpy_d2h": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_d2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_p2p": (ctypes.c_int, [ctypes.c_int, _VP, ctypes.c_int, _VP, ctypes.c_size_t]),
@@ -134,7 +136,8 @@ EXPORTED_SYMBOLS = (
     "sf_last_error", "sf_version", "sf_init", "sf_device_info", "sf_set_stream",
     "sf_get_stream", "sf_device_sync", "sf_alloc", "sf_free", "sf_mem_stats", "sf_trim",
     "sf_reduce_counters", "sf_host_alloc", "sf_host_free",
-    "sf_memcpy_h2d", "sf_memcpy_d2h", "sf_memcpy_d2d", "sf_memcpy_p2p", "sf_elementwise",
+    "sf_memcpy_h2d", "sf_memcpy_h2d_immutable", "sf_memcpy_d2h", "sf_memcpy_d2d",
+    "sf_memcpy_p2p", "sf_elementwise",
     "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
@@ -327,6 +330,32 @@ def upload(dev: int, arr: np.ndarray) -> DeviceBuffer:
     return buf
 
 
+def pooled_pinned(arr: np.ndarray) -> bool:
+    """True when arr views a block of the pinned result pool (an array a
+    download returned): its memory is only reused by a later copy on a
+    device stream, or freed after a device sync (_PinnedPool.put)."""
+    b = arr
+    while isinstance(b, np.ndarray):
+        b = b.base
+    return getattr(b, "_blk", None) is not None
+
+
+def upload_immutable(dev: int, arr: np.ndarray) -> DeviceBuffer:
+    """Upload a read-only C-contiguous array that the caller keeps alive (the
+    new tensor holds it as its host copy): page-locked memory is DMA'd
+    without waiting for the copy.  Later work on the device's stream is
+    ordered after it; a pooled pinned block only returns to the pool when the
+    array dies, and its next use is a copy on the same stream."""
+    buf = alloc(dev, arr.nbytes)
+    if arr.nbytes:
+        flag = ctypes.c_int(0)
+        rc = _lib.sf_memcpy_h2d_immutable(dev, buf.ptr, arr.ctypes.data, arr.nbytes,
+                                          ctypes.byref(flag))
+        if rc:
+            raise _err(_lib, rc, "sf_memcpy_h2d_immutable")
+    return buf
+
+
 class _PinnedBlock:
     """A page-locked host block; returns itself to the pool when the numpy
     array built over it is collected."""
@@ -380,6 +409,10 @@ class _PinnedPool:
                 self.free.setdefault(blk.cap, []).append(ptr)
                 self.cached += blk.cap
                 return
+        # the block may still be the source of an asynchronous upload
+        # (upload_immutable): let every device drain before unpinning it
+        for dev in range(device_count()):
+            _lib.sf_device_sync(dev)
         _lib.sf_host_free(ptr)
 
 

@@ -347,6 +347,24 @@ int sf_host_free(void* p) {
   return SF_OK;
 }
 
+int sf_memcpy_h2d_immutable(int dev, void* dst, const void* src, size_t bytes, int* async) {
+  // The caller guarantees src is immutable and outlives the transfer: a
+  // page-locked source is DMA'd asynchronously (no wait), anything else takes
+  // the regular path.
+  if (async) *async = 0;
+  if (bytes == 0) return SF_OK;
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+    SF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, d->stream));
+    if (async) *async = 1;
+    return SF_OK;
+  }
+  (void)cudaGetLastError();
+  return sf_memcpy_h2d(dev, dst, src, bytes);
+}
+
 int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes) {
   if (bytes == 0) return SF_OK;
   Device* d;
