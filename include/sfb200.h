@@ -90,6 +90,10 @@ int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes);
  * stageflow/tensor.py:138-162. */
 int sf_memcpy_h2d_immutable(int dev, void* dst, const void* src, size_t bytes, int* async);
 int sf_memcpy_d2h(int dev, void* dst, const void* src, size_t bytes);
+/* d2h into page-locked memory, enqueued only: complete once any later
+ * synchronising call on the device's stream returns (used to read a call's
+ * small sibling outputs in the same round trip as the one asked for). */
+int sf_memcpy_d2h_enqueue(int dev, void* dst, const void* src, size_t bytes);
 int sf_memcpy_d2d(int dev, void* dst, const void* src, size_t bytes);
 int sf_memcpy_p2p(int dst_dev, void* dst, int src_dev, const void* src, size_t bytes);
 

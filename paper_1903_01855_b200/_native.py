@@ -67,6 +67,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_memcpy_h2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_h2d_immutable": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t,
                                                    ctypes.POINTER(ctypes.c_int)]),
+        "sf_memcpy_d2h_enqueue": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_d2h": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_d2d": (ctypes.c_int, [ctypes.c_int, _VP, _VP, ctypes.c_size_t]),
         "sf_memcpy_p2p": (ctypes.c_int, [ctypes.c_int, _VP, ctypes.c_int, _VP, ctypes.c_size_t]),
@@ -136,7 +137,8 @@ EXPORTED_SYMBOLS = (
     "sf_last_error", "sf_version", "sf_init", "sf_device_info", "sf_set_stream",
     "sf_get_stream", "sf_device_sync", "sf_alloc", "sf_free", "sf_mem_stats", "sf_trim",
     "sf_reduce_counters", "sf_host_alloc", "sf_host_free",
-    "sf_memcpy_h2d", "sf_memcpy_h2d_immutable", "sf_memcpy_d2h", "sf_memcpy_d2d",
+    "sf_memcpy_h2d", "sf_memcpy_h2d_immutable", "sf_memcpy_d2h", "sf_memcpy_d2h_enqueue",
+    "sf_memcpy_d2d",
     "sf_memcpy_p2p", "sf_elementwise",
     "sf_reduce", "sf_matmul", "sf_transpose2d", "sf_fill", "sf_eye", "sf_cast", "sf_rng_seed",
     "sf_rng_reserve", "sf_rng", "sf_dropout", "sf_jit_compile", "sf_jit_log", "sf_jit_launch",
@@ -437,6 +439,24 @@ def download(buf: DeviceBuffer, np_dtype, shape) -> np.ndarray:
         rc = _lib.sf_memcpy_d2h(buf.dev, out.ctypes.data, buf.ptr, out.nbytes)
         if rc:
             raise _err(_lib, rc, "sf_memcpy_d2h")
+    return out
+
+
+def download_enqueue(buf: DeviceBuffer, np_dtype, shape) -> Optional[np.ndarray]:
+    """Enqueue a device->host copy into a pooled page-locked array without
+    waiting; the array is valid once a later synchronising call on the
+    device's stream has returned.  None when no pinned block is available."""
+    nbytes = int(np.prod(shape, dtype=np.int64)) * np.dtype(np_dtype).itemsize
+    if not (_PinnedPool.MIN <= nbytes <= _PinnedPool.MAX_ARRAY):
+        return None
+    blk = _PINNED.get(nbytes)
+    if blk is None:
+        return None
+    cbuf = (ctypes.c_char * nbytes).from_address(blk.ptr)
+    cbuf._blk = blk
+    out = np.frombuffer(cbuf, dtype=np_dtype).reshape(shape)
+    if _lib.sf_memcpy_d2h_enqueue(buf.dev, blk.ptr, buf.ptr, nbytes):
+        return None
     return out
 
 

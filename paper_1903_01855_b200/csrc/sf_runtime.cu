@@ -418,6 +418,21 @@ int sf_memcpy_h2d(int dev, void* dst, const void* src, size_t bytes) {
   return SF_OK;
 }
 
+int sf_memcpy_d2h_enqueue(int dev, void* dst, const void* src, size_t bytes) {
+  // dst must be page-locked; the copy completes with the stream's next sync
+  if (bytes == 0) return SF_OK;
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, dst) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+    (void)cudaGetLastError();
+    set_error("sf_memcpy_d2h_enqueue: destination is not page-locked host memory");
+    return SF_ERR_INVALID;
+  }
+  SF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, d->stream));
+  return SF_OK;
+}
+
 int sf_memcpy_d2h(int dev, void* dst, const void* src, size_t bytes) {
   Device* d;
   SF_TRY(ensure_device(dev, &d));

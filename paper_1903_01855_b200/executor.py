@@ -516,7 +516,12 @@ class Program:
                     ptrs.append(h._storage_ptr())  # Variable
             raw = plan.run(ptrs)
             dev, device, DB, adopt = self.dev, self.device, _native.DeviceBuffer, Tensor._adopt
-            return [adopt(dt, shape, device, DB(dev, raw[j], nb)) for j, nb, dt, shape in specs]
+            outs = [adopt(dt, shape, device, DB(dev, raw[j], nb)) for j, nb, dt, shape in specs]
+            if len(outs) > 1:
+                sib = [weakref.ref(t) for t in outs]
+                for t in outs:
+                    t._sib = sib
+            return outs
         env: Dict[int, object] = {}
         for lv, v in zip(self.in_vals, inputs):
             env[id(lv)] = v

@@ -53,6 +53,27 @@ def test_read_only_pinned_result_uploads_asynchronously():
     np.testing.assert_array_equal(t2.numpy(), base)
 
 
+def test_reading_one_output_reads_small_siblings_in_the_same_round_trip():
+    rng = np.random.default_rng(2)
+    xa = rng.standard_normal((50000, 2)).astype(np.float32)
+
+    @sf.stage
+    def f(x):
+        return sf.mul(x, 2.0), sf.reduce_sum(sf.exp(x), axes=(1,))
+
+    x = sf.constant(xa)
+    for _ in range(2):  # second call: the traced program is warm
+        a, b = f(x)
+    ha = a.numpy()
+    assert b._pend is not None          # enqueued with a's read
+    hb = b.numpy()
+    assert b._pend is None
+    np.testing.assert_array_equal(ha, xa * np.float32(2.0))
+    np.testing.assert_allclose(hb, np.exp(xa.astype(np.float64)).sum(1), rtol=1e-6)
+    a2, b2 = f(x)
+    assert b2.raw().tobytes() == hb.tobytes() and not b2.raw().flags.writeable
+
+
 def test_listing_square_and_nested():
     x = sf.constant(3.0)
     with sf.Tape() as t1:
