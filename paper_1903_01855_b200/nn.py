@@ -151,6 +151,25 @@ def _conv_grads_infer(attrs, in_specs, env=None):
     return [in_specs[0], in_specs[1]]
 
 
+def _narrow_conv_grads(gf, node, used):
+    """conv2d_grads with one gradient unread -> the single-gradient op (e.g.
+    the first layer's gradient w.r.t. the input images, which a training step
+    never reads: no data-gradient GEMM and no col2im for it)."""
+    from .graph import Node
+
+    x_ref, w_ref, dy_ref = node.inputs
+    a = {"stride": node.attrs["stride"], "pad": node.attrs["pad"]}
+    if used == {1}:
+        attrs = dict(sorted(dict(a, filter_shape=tuple(gf.spec_of(w_ref)[1])).items()))
+        return (Node("conv2d_grad_filter", (x_ref, dy_ref), attrs, node.device,
+                     (node.out_specs[1],)), {1: 0})
+    if used == {0}:
+        attrs = dict(sorted(dict(a, input_shape=tuple(gf.spec_of(x_ref)[1])).items()))
+        return (Node("conv2d_grad_input", (dy_ref, w_ref), attrs, node.device,
+                     (node.out_specs[0],)), {0: 0})
+    return None
+
+
 def _conv_grads_kernel(attrs, inputs, env):
     x, w, dy = inputs
     _check_float("conv2d_grads", x, w, dy)
@@ -338,6 +357,9 @@ def install() -> None:
     from .executor import GRAPH_SAFE_OPS
 
     plugins.install()
+    from .graph import OUTPUT_NARROWING
+
+    OUTPUT_NARROWING["conv2d_grads"] = _narrow_conv_grads
     reg = get_runtime().registry
     for d in nn_defs():
         try:

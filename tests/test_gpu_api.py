@@ -53,6 +53,36 @@ def test_read_only_pinned_result_uploads_asynchronously():
     np.testing.assert_array_equal(t2.numpy(), base)
 
 
+def test_staged_backward_computes_only_gradients_that_can_be_read():
+    """A tape over a staged call asks its backward only for gradients that
+    can reach a requested source: the input images' gradient is pruned and
+    conv2d_grads narrows to the filter gradient; results are unchanged."""
+    from paper_1903_01855_b200 import nn
+    from paper_1903_01855_b200.backprop import get_forward_backward
+
+    nn.install()
+    rng = np.random.default_rng(4)
+    x = sf.constant(rng.standard_normal((2, 9, 9, 8)).astype(np.float32))
+    w = sf.Variable(sf.constant(rng.standard_normal((3, 3, 8, 4)).astype(np.float32)))
+
+    def loss(x):
+        return sf.reduce_sum(nn.conv2d(x, w.read_value(), stride=1, pad=1))
+
+    staged = sf.stage(loss)
+    grads = []
+    for f in (loss, staged):
+        with sf.Tape() as t:
+            val = f(x)
+        grads.append(t.gradient(val, [w])[0].numpy())
+    np.testing.assert_allclose(grads[1], grads[0], rtol=1e-5, atol=1e-4)
+    cf = staged.cached_functions()[0]
+    bwd = get_forward_backward(cf.graph)[1]
+    sel = list(getattr(bwd, "_selected", {}).values())
+    assert sel, "the backward was not restricted to the readable gradients"
+    ops_used = {n.op for n in sel[0].graph.nodes}
+    assert "conv2d_grad_filter" in ops_used and "conv2d_grads" not in ops_used
+
+
 def test_reading_one_output_reads_small_siblings_in_the_same_round_trip():
     rng = np.random.default_rng(2)
     xa = rng.standard_normal((50000, 2)).astype(np.float32)
