@@ -369,6 +369,51 @@ __global__ void maxpool_gather_kernel(const signed char* __restrict__ am,
   }
 }
 
+// The same gather for float32 with C % 4 == 0: a thread owns 4 channels of
+// one input pixel (char4 argmax / float4 gradient loads) and visits only the
+// windows that contain the pixel, computed from the geometry instead of
+// testing all K x K taps with divisions; windows are visited in the order of
+// maxpool_gather_kernel (kh, then kw ascending), so sums are bit-identical.
+__global__ void __launch_bounds__(256) maxpool_gather_f32x4_kernel(
+    const signed char* __restrict__ am, const float* __restrict__ dy, float* __restrict__ dx,
+    ConvGeom g) {
+  const int C4 = (int)g.c / 4, W = (int)g.w, H = (int)g.h, WO = (int)g.wo, HO = (int)g.ho;
+  const int S = (int)g.s, P = (int)g.p, KH = (int)g.kh, KW = (int)g.kw;
+  const int total = (int)(g.n * g.h * g.w) * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4, t = i / C4;
+    const int w = t % W, t2 = t / W;
+    const int h = t2 % H, n = t2 / H;
+    // windows oh with oh*S - P <= h <= oh*S - P + KH - 1; kh = h + P - oh*S
+    const int yh = h + P, xw = w + P;
+    const int oh_hi = min(HO - 1, yh / S), ow_hi = min(WO - 1, xw / S);
+    const int oh_lo = yh - KH + 1 <= 0 ? 0 : (yh - KH + S) / S;
+    const int ow_lo = xw - KW + 1 <= 0 ? 0 : (xw - KW + S) / S;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    bool any[4] = {false, false, false, false};
+    for (int oh = oh_hi; oh >= oh_lo; --oh) {  // kh ascending
+      const int kh = yh - oh * S;
+      for (int ow = ow_hi; ow >= ow_lo; --ow) {  // kw ascending
+        const int kw = xw - ow * S;
+        const int o4 = ((n * HO + oh) * WO + ow) * C4 + c4;
+        const char4 m = reinterpret_cast<const char4*>(am)[o4];
+        const signed char tap = (signed char)(kh * KW + kw);
+        if (m.x != tap && m.y != tap && m.z != tap && m.w != tap) continue;
+        const float4 v = reinterpret_cast<const float4*>(dy)[o4];
+        const signed char mm[4] = {m.x, m.y, m.z, m.w};
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (mm[e] == tap) {
+            a[e] = any[e] ? sf::add(a[e], vv[e]) : vv[e];
+            any[e] = true;
+          }
+      }
+    }
+    reinterpret_cast<float4*>(dx)[i] = make_float4(a[0], a[1], a[2], a[3]);
+  }
+}
+
 // softmax cross-entropy per row: loss = log(sum exp(x - m)) + m - x[label];
 // one warp per row; the sum follows the canonical reduction order.
 template <class T>
@@ -571,8 +616,12 @@ int sf_maxpool2d_grad(int dev, int dtype, const int64_t* g8, const void* x, cons
     const int st = by_dtype(dtype, [&](auto t) {
       using T = decltype(t);
       maxpool_argmax_kernel<T><<<grid_for_n(d, outs), 256, 0, d->stream>>>((const T*)x, am, g);
-      maxpool_gather_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>(
-          am, (const T*)dy, (T*)*dx, g);
+      if (std::is_same<T, float>::value && g.c % 4 == 0)
+        maxpool_gather_f32x4_kernel<<<grid_for_n(d, total / 4), 256, 0, d->stream>>>(
+            am, (const float*)dy, (float*)*dx, g);
+      else
+        maxpool_gather_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>(
+            am, (const T*)dy, (T*)*dx, g);
       SF_CHECK_CUDA(cudaGetLastError());
       return SF_OK;
     });

@@ -62,6 +62,25 @@ def test_conv_weight_grad_split_k():
     np.testing.assert_allclose(gw, want, rtol=1e-4, atol=2e-3)
 
 
+@pytest.mark.parametrize("shape,k,s,p", [((2, 9, 9, 8), 3, 2, 1), ((2, 10, 7, 64), 3, 1, 1),
+                                         ((1, 12, 12, 4), 2, 2, 0), ((3, 8, 8, 12), 3, 2, 0)])
+def test_maxpool_grad_vectorised_vs_oracle(shape, k, s, p):
+    """The 4-channel gather (C % 4 == 0) visits exactly the windows holding
+    each pixel; ties and overlapping windows (the argmax of several windows)
+    accumulate like the oracle."""
+    rng = np.random.default_rng(3)
+    x = rng.integers(-3, 3, size=shape).astype(np.float32)  # many ties
+    tx = sf.constant(x)
+    with sf.Tape() as t:
+        t.watch(tx)
+        y = nn.max_pool(tx, k, s, p)
+        dy = rng.standard_normal(y.shape).astype(np.float32)
+        loss = sf.reduce_sum(sf.mul(y, sf.constant(dy)))
+    np.testing.assert_array_equal(y.numpy(), nn_np.max_pool(x, k, s, p))
+    np.testing.assert_allclose(t.gradient(loss, tx).numpy(), nn_np.max_pool_grad(x, dy, k, s, p),
+                               rtol=1e-6, atol=1e-6)
+
+
 def test_maxpool_and_xent_vs_oracle():
     rng = np.random.default_rng(1)
     x = rng.standard_normal((2, 9, 9, 3)).astype(np.float32)
