@@ -163,21 +163,26 @@ __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, Con
 
 // im2col fused with the 3xTF32 hi/lo split and K padding (row stride kp):
 // feeds the tcgen05 GEMM directly (csrc/sf_gemm_tc.cu)
+// I: index type — int (32-bit division, several times cheaper) whenever the
+// matrix and the input have < 2^31 elements (every ResNet layer), else long long
+template <class I>
 __global__ void im2col_split_kernel(const float* __restrict__ x, float* __restrict__ hi,
-                                    float* __restrict__ lo, ConvGeom g, long long kp) {
-  const long long K = g.kh * g.kw * g.c;
-  const long long total = g.n * g.ho * g.wo * kp;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
-    const long long k = i % kp, m = i / kp;
+                                    float* __restrict__ lo, ConvGeom g, long long kp_) {
+  const I kp = (I)kp_, C = (I)g.c, KW = (I)g.kw, WO = (I)g.wo, HO = (I)g.ho;
+  const I H = (I)g.h, W = (I)g.w, S = (I)g.s, P = (I)g.p;
+  const I K = (I)g.kh * KW * C;
+  const I total = (I)(g.n * g.ho * g.wo) * kp;
+  const I stride = (I)gridDim.x * blockDim.x;
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const I m = i / kp, k = i - m * kp;
     float v = 0.f;
     if (k < K) {
-      const long long c = k % g.c, t = k / g.c;
-      const long long kw = t % g.kw, kh = t / g.kw;
-      const long long ow = m % g.wo, t2 = m / g.wo;
-      const long long oh = t2 % g.ho, n = t2 / g.ho;
-      const long long ih = oh * g.s - g.p + kh, iw = ow * g.s - g.p + kw;
-      if (ih >= 0 && ih < g.h && iw >= 0 && iw < g.w) v = x[((n * g.h + ih) * g.w + iw) * g.c + c];
+      const I t = k / C, c = k - t * C;
+      const I kh = t / KW, kw = t - kh * KW;
+      const I t2 = m / WO, ow = m - t2 * WO;
+      const I n = t2 / HO, oh = t2 - n * HO;
+      const I ih = oh * S - P + kh, iw = ow * S - P + kw;
+      if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((n * H + ih) * W + iw) * C + c];
     }
     if (lo == nullptr) {  // raw padded cols (the GEMM derives lo in shared memory)
       hi[i] = v;
@@ -554,8 +559,11 @@ int sf_im2col_split(int dev, const int64_t* g8, int64_t kp, const void* x, void*
     else
       im2col_seg_kernel<float, false><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
           (const float*)x, (float*)*hi, nullptr, g, (int)kp);
+  } else if (total < (1ll << 31) - (1ll << 24) && g.n * g.h * g.w * g.c < (1ll << 31)) {
+    im2col_split_kernel<int><<<grid_for_n(d, total), 256, 0, d->stream>>>(
+        (const float*)x, (float*)*hi, lo ? (float*)*lo : nullptr, g, kp);
   } else {
-    im2col_split_kernel<<<grid_for_n(d, total), 256, 0, d->stream>>>(
+    im2col_split_kernel<long long><<<grid_for_n(d, total), 256, 0, d->stream>>>(
         (const float*)x, (float*)*hi, lo ? (float*)*lo : nullptr, g, kp);
   }
   SF_CHECK_CUDA(cudaGetLastError());
