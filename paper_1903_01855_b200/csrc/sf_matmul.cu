@@ -121,7 +121,12 @@ __global__ void gemm_small(const T* __restrict__ A, const T* __restrict__ B, T* 
 
 template <class T, bool TA, bool TB>
 static void gemm_go(Device* d, const T* A, const T* B, T* C, long long m, long long n, long long k) {
-  if ((m * n <= 4096 && k <= 256) || k <= 8) {
+  const long long tiles64 = ((n + 63) / 64) * ((m + 63) / 64);
+  // one thread per output also when the 64x64 tiling would leave most SMs
+  // idle (a classifier layer: m = batch, n = 1000, k = 2048 -> 16 tiles) and
+  // there are enough outputs to fill them; the k order is the same
+  const bool few_tiles = tiles64 * 2 < d->sm_count && m * n >= 8192 && k < 16384;
+  if ((m * n <= 4096 && k <= 256) || k <= 8 || few_tiles) {
     long long blocks = (m * n + 255) / 256;
     if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
     if (blocks < 1) blocks = 1;
