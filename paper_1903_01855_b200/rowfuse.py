@@ -39,9 +39,12 @@ MIN_BATCH = 2
 # program is cut into chunks of about this many scalar operations; each
 # chunk is its own kernel (rowed values crossing a cut round-trip through
 # L2-resident temporaries) and the chunks compile in parallel.
-# (B200 sweep, tools/sweep_rows.sh, L2HMC 1e5 chains: 1200 -> 0.38 ms/step,
-# 4800 -> 0.29 ms, 9600 -> 0.28 ms but 3x the compile time, 19200+ slower.)
-CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "4800"))
+# (B200 sweeps, tools/sweep_rows.sh, L2HMC 1e5 chains, before re-rolling:
+# 1200 -> 0.38 ms/step, 4800 -> 0.29 ms, 9600 -> 0.28 ms at 3x the compile
+# time, 19200+ slower.  With re-rolled loops the whole transition is ~9000
+# ops: 4800 -> 2 row kernels, 0.202 ms; 9000 -> 1 row kernel, 0.196 ms, and
+# 0.081 -> 0.077 ms at 200 chains, for +1.3 s of one-time compile (cached).)
+CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "9000"))
 # CTAs of 128 threads that must fit per SM (register budget = 64K / (128 *
 # MIN_BLOCKS)); 0 = no minimum, ptxas picks (best in the sweep once the
 # weights are read with volatile vector loads: ~96 registers, no spills)
