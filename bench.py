@@ -323,8 +323,19 @@ def run_ours(a, rank, world, dist):
     jit_ms = [ms / runs for kind, ms, runs in stats if kind == 1 and runs]
     kern_ms = sum(jit_ms)
     achieved = flops_per_step / (kern_ms / 1e3) / 1e12 if kern_ms else 0.0
+    # DRAM bytes per launch of the row kernel, from the committed ncu --set
+    # full capture of this configuration (profiles/r01i_l2hmc_rows_full.md)
+    traffic = None
+    try:
+        tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                          "r01i_rows_traffic.json")
+        with open(tp) as fh:
+            traffic = json.load(fh)["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "fp32", "achieved": achieved, "peak": FFMA_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FFMA_PEAK_TFLOPS, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / FFMA_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per row-kernel launch (ncu)",
                 "peak_kind": "derived nominal FP32 SIMT (148 SM x 128 lanes x 2 x 1.965 GHz); "
                              "the row program has no tensor-core-shaped work (K<=10 per chain)",
                 "kernels_per_step": len(jit_ms), "kernel_ms_per_step": kern_ms,
