@@ -250,12 +250,20 @@ class Program:
                           if last_use.get(id(o), -1) > u}
                 n_launch += self._emit_rows(pw, unit, needed, slot_for_use, slot_for_def)
             elif isinstance(unit, FusedGroup):
-                needed = set()
+                needed = set(unit.inplace)  # variable updates are always stored
                 for op in unit.ops:
                     o = op.outs[0]
                     if last_use.get(id(o), -1) > u:
                         needed.add(id(o))
-                n_launch += self._emit_group(pw, unit, needed, slot_for_use, slot_for_def)
+                inplace = unit.inplace
+
+                def group_def(o, _inplace=inplace):
+                    # an in-place variable update writes the variable's buffer
+                    v = _inplace.get(id(o))
+                    return slot_for_use(v) if v is not None else slot_for_def(o)
+
+                n_launch += self._emit_group(pw, unit, needed, slot_for_use,
+                                             group_def if inplace else slot_for_def)
             else:
                 n_launch += self._emit_op(pw, unit, slot_for_use, slot_for_def)
         pw.n_inputs = len(in_roots)

@@ -262,7 +262,7 @@ def _splat_value(t: Tensor):
 
 
 class FusedGroup:
-    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs", "vec", "reduces")
+    __slots__ = ("ops", "shape", "outs_needed", "ext_inputs", "vec", "reduces", "inplace")
 
     def __init__(self, shape):
         self.ops: List[LOp] = []
@@ -271,6 +271,7 @@ class FusedGroup:
         self.ext_inputs: List[LV] = []
         self.vec = 1  # elements per thread of the generated kernel
         self.reduces: List[LOp] = []  # column reductions folded in (fuse_reductions)
+        self.inplace: Dict[int, LV] = {}  # id(out) -> variable it is stored into (var_add)
 
 
 _PURE_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "eye"))
@@ -321,6 +322,8 @@ def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
     units: List[Any] = []
     produced_at: Dict[int, int] = {}
     latest: Dict[tuple, int] = {}  # shape -> index of the latest group of that shape
+    var_touch: Dict[int, int] = {}  # id(variable) -> unit index of its last access
+    barrier = -1                    # unit index of the last Python-executed op
 
     def record(unit_ops, u):
         for o_op in unit_ops:
@@ -332,6 +335,24 @@ def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
             units.append(op)
             record(op[0].ops, len(units) - 1)
             continue
+        if op.kind == "var_add" and fuse_enabled and FUSE_UPDATES:
+            # v += x with x computed by an earlier group of v's shape: the
+            # group stores v + x into v itself (one launch instead of two);
+            # legal when nothing touched v since that group ran
+            v, x = op.ins
+            g = produced_at.get(id(x.root()), -1)
+            grp = units[g] if g >= 0 else None
+            if (isinstance(grp, FusedGroup) and x.root() is x and v.root() is v
+                    and tuple(grp.shape) == tuple(v.shape) == tuple(x.shape)
+                    and v.dtype is x.dtype and v.dtype in _VEC4
+                    and var_touch.get(id(v), -1) < g and barrier < g):
+                o = LV(-1, v.dtype, v.shape, "op")
+                upd = LOp("ew", "add", [v, x], [o])
+                o.producer = upd
+                grp.ops.append(upd)
+                grp.inplace[id(o)] = v
+                var_touch[id(v)] = g
+                continue
         if op.kind == "ew" and fuse_enabled:
             shape = tuple(op.outs[0].shape)
             g = latest.get(shape)
@@ -347,7 +368,14 @@ def fuse(ops: List[LOp], fuse_enabled: bool) -> List[Any]:
             continue
         units.append(op)
         record([op], len(units) - 1)
+        if op.kind in ("var_read", "var_assign", "var_add") and op.ins:
+            var_touch[id(op.ins[0].root())] = len(units) - 1
+        elif op.kind == "py":
+            barrier = len(units) - 1
     return units
+
+
+FUSE_UPDATES = True  # var_add folded into the group computing its increment
 
 
 # ---------------------------------------------------------------------------

@@ -121,3 +121,21 @@ def test_fused_sources_compile():
     name, src, ext, outs = lowering.generate_group(g, {id(g.ops[0].outs[0])})
     assert g.vec == 4 and "float4" in src
     _native.jit_compile(name, src)
+
+
+def test_variable_update_folds_into_increment_group_unless_touched():
+    P = _Prog()
+    g = P.lv((32, 8), "input")
+    v = P.lv((32, 8), "var")
+    w = P.lv((32, 8), "var")
+    inc = P.op("ew", "mul", [g, g], (32, 8))
+    P.ops.append(LOp("var_add", "var_add", [v, inc], []))
+    P.ops.append(LOp("var_read", "var_read", [w], [P.lv((32, 8))]))  # touches w only
+    inc2 = P.op("ew", "mul", [g, inc], (32, 8))
+    P.ops.append(LOp("var_add", "var_add", [w, inc2], []))  # w read after inc2's group: kept
+    units = lowering.fuse(P.ops, True)
+    groups = [u for u in units if isinstance(u, FusedGroup)]
+    assert list(groups[0].inplace.values()) == [v]
+    assert [op.name for op in groups[0].ops] == ["mul", "add", "mul"]
+    # w's update: w was read after the group ran, so it stays a separate op
+    assert any(isinstance(u, LOp) and u.kind == "var_add" for u in units)

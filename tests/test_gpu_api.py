@@ -53,6 +53,35 @@ def test_read_only_pinned_result_uploads_asynchronously():
     np.testing.assert_array_equal(t2.numpy(), base)
 
 
+def test_staged_variable_updates_fold_into_groups_bitwise():
+    """v.assign_add(g * -lr) for several same-shape variables: the staged
+    program stores v + increment from the group that computes the increment
+    (in place); values match eager bit for bit, and a read after the update
+    inside the same function sees the new value."""
+    rng = np.random.default_rng(8)
+    shapes = [(64, 32), (64, 32), (128,)]
+    init = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    grads = [sf.constant(rng.standard_normal(s).astype(np.float32)) for s in shapes]
+
+    def run(staged):
+        vs = [sf.Variable(sf.constant(a)) for a in init]
+
+        def update(*gs):
+            for v, g in zip(vs, gs):
+                v.assign_add(sf.mul(g, -0.125))
+            return sf.reduce_sum(sf.mul(vs[0].read_value(), 2.0))
+
+        f = sf.stage(update) if staged else update
+        outs = [f(*grads).numpy() for _ in range(3)]
+        return [v.read_value().numpy() for v in vs], outs
+
+    (ve, oe), (vs_, os_) = run(False), run(True)
+    for a, b in zip(ve, vs_):
+        assert a.tobytes() == b.tobytes()
+    for a, b in zip(oe, os_):
+        assert a.tobytes() == b.tobytes()
+
+
 def test_staged_backward_computes_only_gradients_that_can_be_read():
     """A tape over a staged call asks its backward only for gradients that
     can reach a requested source: the input images' gradient is pruned and
