@@ -163,6 +163,37 @@ __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, Con
 
 // im2col fused with the 3xTF32 hi/lo split and K padding (row stride kp):
 // feeds the tcgen05 GEMM directly (csrc/sf_gemm_tc.cu)
+// Raw im2col rows when C is not a multiple of 4 (the 3-channel stem): one
+// warp per output row m, the row's pixel decoded once, lanes walk k so every
+// store is a coalesced 128-byte line (the element-per-thread kernel below
+// re-decoded m for every element and stored with a stride of kp).
+__global__ void __launch_bounds__(256) im2col_rows_kernel(const float* __restrict__ x,
+                                                          float* __restrict__ out, ConvGeom g,
+                                                          int kp) {
+  const int C = (int)g.c, KW = (int)g.kw, WO = (int)g.wo, HO = (int)g.ho;
+  const int H = (int)g.h, W = (int)g.w, S = (int)g.s, P = (int)g.p;
+  const int K = (int)g.kh * KW * C, M = (int)(g.n * g.ho * g.wo);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; m < M; m += nwarps) {
+    const int t2 = m / WO, ow = m - t2 * WO;
+    const int n = t2 / HO, oh = t2 - n * HO;
+    const int ih0 = oh * S - P, iw0 = ow * S - P;
+    const float* xn = x + (long long)n * H * W * C;
+    float* row = out + (long long)m * kp;
+    for (int k = lane; k < kp; k += 32) {
+      float v = 0.f;
+      if (k < K) {
+        const int t = k / C, c = k - t * C;
+        const int kh = t / KW, kw = t - kh * KW;
+        const int ih = ih0 + kh, iw = iw0 + kw;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = xn[(ih * W + iw) * C + c];
+      }
+      row[k] = v;
+    }
+  }
+}
+
 // I: index type — int (32-bit division, several times cheaper) whenever the
 // matrix and the input have < 2^31 elements (every ResNet layer), else long long
 template <class I>
@@ -559,6 +590,9 @@ int sf_im2col_split(int dev, const int64_t* g8, int64_t kp, const void* x, void*
     else
       im2col_seg_kernel<float, false><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
           (const float*)x, (float*)*hi, nullptr, g, (int)kp);
+  } else if (!lo && total < (1ll << 31) - (1ll << 24) && g.n * g.h * g.w * g.c < (1ll << 31)) {
+    im2col_rows_kernel<<<grid_for_n(d, g.n * g.ho * g.wo * 32), 256, 0, d->stream>>>(
+        (const float*)x, (float*)*hi, g, (int)kp);
   } else if (total < (1ll << 31) - (1ll << 24) && g.n * g.h * g.w * g.c < (1ll << 31)) {
     im2col_split_kernel<int><<<grid_for_n(d, total), 256, 0, d->stream>>>(
         (const float*)x, (float*)*hi, lo ? (float*)*lo : nullptr, g, kp);
