@@ -374,6 +374,23 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// split-K epilogue, 16-byte accesses (mn % 4 == 0): same split order
+__global__ void splitk_reduce_x4(const float4* __restrict__ W, float4* __restrict__ C,
+                                 long long mn4, int splits) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mn4; i += stride) {
+    float4 acc = W[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = W[(long long)s * mn4 + i];
+      acc.x = acc.x + v.x;
+      acc.y = acc.y + v.y;
+      acc.z = acc.z + v.z;
+      acc.w = acc.w + v.w;
+    }
+    C[i] = acc;
+  }
+}
+
 // split-K epilogue: sum of the partial tiles in split order (deterministic)
 __global__ void splitk_reduce(const float* __restrict__ W, float* __restrict__ C, long long mn,
                               int splits) {
@@ -537,9 +554,16 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
     SF_CHECK_CUDA(cudaGetLastError());
     return SF_OK;
   }
-  long long blocks = (M * N + 255) / 256;
-  if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
-  splitk_reduce<<<(unsigned)blocks, 256, 0, d->stream>>>(work, c, M * N, (int)splits);
+  if ((M * N) % 4 == 0 && (uintptr_t)c % 16 == 0) {
+    long long blocks = (M * N / 4 + 255) / 256;
+    if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
+    splitk_reduce_x4<<<(unsigned)blocks, 256, 0, d->stream>>>(
+        (const float4*)work, (float4*)c, M * N / 4, (int)splits);
+  } else {
+    long long blocks = (M * N + 255) / 256;
+    if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
+    splitk_reduce<<<(unsigned)blocks, 256, 0, d->stream>>>(work, c, M * N, (int)splits);
+  }
   count_launch(d->id, 2);
   d->alloc.release(work);  // stream-ordered reuse is safe
   SF_CHECK_CUDA(cudaGetLastError());
