@@ -51,12 +51,13 @@ CHUNK_COST = int(__import__("os").environ.get("SF_CHUNK_COST", "9000"))
 MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
 # chains per thread in row kernels: 0 = automatic.  Measured on B200 (L2HMC,
 # 1e5 chains): 2 chains/thread halves the shared-memory weight loads per
-# chain but needs ~160 registers, so the SM holds half the threads; the
-# chains in flight per SM stay the same and the step time did not move
-# (0.207 vs 0.204 ms).  Automatic therefore keeps 1 (REPLICA_MIN_BATCH is
-# the batch from which 2 would be chosen).
+# chain and doubles the independent work per thread.  With the transition
+# split over two row kernels it did not move the step (0.207 vs 0.204 ms);
+# with the whole transition in one kernel it does: 0.195 -> 0.182 ms
+# (compile 3.7 -> 10 s, one-time, cached).  Automatic picks 2 from
+# REPLICA_MIN_BATCH chains on (enough chains to keep every SM busy).
 ROW_REPLICAS = int(__import__("os").environ.get("SF_ROW_REPLICAS", "0"))
-REPLICA_MIN_BATCH = 1 << 62
+REPLICA_MIN_BATCH = 65536
 # SMs of the target GPU (B200: 148); set by the executor from the device
 SM_COUNT = 148
 # matvec weight vectors loaded ahead of their FMAs (latency hiding vs registers)
