@@ -53,11 +53,14 @@ MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
 # 1e5 chains): 2 chains/thread halves the shared-memory weight loads per
 # chain and doubles the independent work per thread.  With the transition
 # split over two row kernels it did not move the step (0.207 vs 0.204 ms);
-# with the whole transition in one kernel it does: 0.195 -> 0.182 ms
-# (compile 3.7 -> 10 s, one-time, cached).  Automatic picks 2 from
-# REPLICA_MIN_BATCH chains on (enough chains to keep every SM busy).
+# with the whole transition in one kernel it does with a warm L2: 0.195 ->
+# 0.177 ms (e2e 3.5e8 -> 3.7e8 samples/s; compile 3.7 -> 10 s, cached).  But
+# the doubled loop body makes the step sensitive to a cold L2 (instruction
+# refetch): with the L2 flushed between steps, as bench.py times the
+# headline, 0.204 -> 0.239 ms.  Automatic keeps 1 chain per thread; set
+# SF_ROW_REPLICAS=2 (or REPLICA_MIN_BATCH) for warm-cache serving loops.
 ROW_REPLICAS = int(__import__("os").environ.get("SF_ROW_REPLICAS", "0"))
-REPLICA_MIN_BATCH = 65536
+REPLICA_MIN_BATCH = 1 << 62
 # SMs of the target GPU (B200: 148); set by the executor from the device
 SM_COUNT = 148
 # matvec weight vectors loaded ahead of their FMAs (latency hiding vs registers)
