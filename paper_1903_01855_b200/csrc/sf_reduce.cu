@@ -188,14 +188,15 @@ __global__ void __launch_bounds__(XT * 32) reduce_cols_f32x4(const float* __rest
                                                              float* __restrict__ part,
                                                              float* __restrict__ out, int mean,
                                                              float countf,
-                                                             unsigned* __restrict__ counters) {
+                                                             unsigned* __restrict__ counters,
+                                                             int NB) {
   __shared__ float acc_s[32][XT * 4 + 1];
-  // per-thread staging slots [NB][XT * 32] (dynamic, kColsStageBytes): a
+  // per-thread staging slots [NB][XT * 32] (dynamic, NB * XT * 512 bytes): a
   // batch of NB rows is copied with cp.async, so all NB loads are in flight
   // at once — with register loads ptxas interleaves load and add (the fold
   // order is strict) and keeps only 2-3 loads outstanding, which starves
   // HBM on the small grids of wide-channel layers
-  constexpr int NT = XT * 32, NB = 128 / XT;
+  constexpr int NT = XT * 32;
   extern __shared__ float4 stage[];
   const int tx = threadIdx.x, tl = threadIdx.y, tid = tl * XT + tx;
   const long long c0 = ((long long)blockIdx.x * XT + tx) * 4;
@@ -304,12 +305,17 @@ static void launch_cols_x4(Device* d, const float* in, long long R, long long C,
   const unsigned long long bit = 1ull << (d->id & 63);
   if (!(attr_set.load() & bit)) {
     cudaFuncSetAttribute(reduce_cols_f32x4<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kColsStageBytes);
+                         2 * kColsStageBytes);
     attr_set.fetch_or(bit);
   }
   dim3 grid((unsigned)((C / 4 + XT - 1) / XT), (unsigned)n_chunks);
-  reduce_cols_f32x4<XT><<<grid, dim3(XT, 32), kColsStageBytes, d->stream>>>(
-      in, R, C, chunk, n_chunks, part, out, mean, countf, d->red_counters);
+  // a grid of at most one block per SM (narrow late layers): stage a lane's
+  // 32 rows in one batch — one memory round trip instead of two
+  int nb = 128 / XT;
+  if (XT == 8 && (long long)grid.x * grid.y <= d->sm_count) nb = 32;
+  const size_t smem = (size_t)nb * XT * 32 * 16;
+  reduce_cols_f32x4<XT><<<grid, dim3(XT, 32), smem, d->stream>>>(
+      in, R, C, chunk, n_chunks, part, out, mean, countf, d->red_counters, nb);
 }
 
 // One launch: sum (or mean) over the rows of a row-major (R, C) float32
