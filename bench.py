@@ -347,17 +347,15 @@ def run_ours(a, rank, world, dist):
     # -- e2e through the public API: the chain state lives on the host between
     # steps; each step uploads it (H2D from page-locked memory), transitions,
     # and reads the new state and the acceptance back (D2H).  The state read
-    # back is a page-locked array of the result pool; frozen read-only and fed
-    # to the next step, its upload is an asynchronous DMA that overlaps the
+    # back is a page-locked array of the result pool (Tensor.raw: permanently
+    # read-only); fed to the next step, its upload is an asynchronous DMA that overlaps the
     # call's host-side work (tensor_from_host: immutable pinned sources).
-    x_host = sampler.x.numpy()
-    x_host.flags.writeable = False
+    x_host = sampler.x.raw()
 
     def e2e_step(x_host):
         x = sf.tensor_from_host(x_host, (B, 2), sf.float32)   # H2D inside the call
         x_out, acc = sampler.transition(x)
-        xo, ao = x_out.numpy(), acc.numpy()                   # D2H of the step's results
-        xo.flags.writeable = False
+        xo, ao = x_out.raw(), acc.raw()                       # D2H of the step's results
         return xo
 
     for _ in range(a.warmup):

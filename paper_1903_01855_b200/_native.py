@@ -332,14 +332,33 @@ def upload(dev: int, arr: np.ndarray) -> DeviceBuffer:
     return buf
 
 
-def pooled_pinned(arr: np.ndarray) -> bool:
-    """True when arr views a block of the pinned result pool (an array a
-    download returned): its memory is only reused by a later copy on a
-    device stream, or freed after a device sync (_PinnedPool.put)."""
+def frozen_pinned(arr: np.ndarray) -> bool:
+    """True when arr views a block of the pinned result pool through a
+    read-only memoryview the runtime put there (``freeze_pinned``): nothing
+    can make it writable again, and its memory is only reused by a later
+    copy on a device stream, or freed after a device sync (_PinnedPool)."""
+    b, ro = arr, False
+    while True:
+        if isinstance(b, np.ndarray):
+            b = b.base
+        elif isinstance(b, memoryview):
+            ro = ro or b.readonly
+            b = b.obj
+        else:
+            break
+    return ro and getattr(b, "_blk", None) is not None
+
+
+def freeze_pinned(arr: np.ndarray) -> np.ndarray:
+    """A permanently read-only view of a pinned-pool download (Tensor.raw):
+    its WRITEABLE flag can never be set again, so uploading it may alias it."""
     b = arr
     while isinstance(b, np.ndarray):
         b = b.base
-    return getattr(b, "_blk", None) is not None
+    if getattr(b, "_blk", None) is None or not arr.flags.c_contiguous:
+        arr.flags.writeable = False
+        return arr
+    return np.frombuffer(memoryview(arr).toreadonly(), dtype=arr.dtype).reshape(arr.shape)
 
 
 def upload_immutable(dev: int, arr: np.ndarray) -> DeviceBuffer:
@@ -387,20 +406,30 @@ class _PinnedPool:
         self.free: dict = {}
         self.cached = 0
         self.lock = threading.Lock()
+        # blocks over LIMIT waiting to be unpinned.  put() runs from a
+        # finalizer (any allocation can trigger it, including one inside a
+        # stream capture), so it never syncs or frees: drain() does, from
+        # get() -- called only outside captures.
+        self.pending: list = []
 
     def get(self, nbytes: int) -> Optional["_PinnedBlock"]:
         cap = self.MIN
         while cap < nbytes:
             cap <<= 1
+        if self.pending:
+            self.drain()
+        ptr = 0
         with self.lock:
             lst = self.free.get(cap)
             if lst:
                 self.cached -= cap
-                return _PinnedBlock(lst.pop(), cap)
-        p = ctypes.c_void_p(0)
-        if _lib.sf_host_alloc(cap, ctypes.byref(p)):
-            return None
-        return _PinnedBlock(p.value, cap)
+                ptr = lst.pop()
+        if not ptr:
+            p = ctypes.c_void_p(0)
+            if _lib.sf_host_alloc(cap, ctypes.byref(p)):
+                return None
+            ptr = p.value
+        return _PinnedBlock(ptr, cap)  # created outside the lock (see put)
 
     def put(self, blk: "_PinnedBlock") -> None:
         ptr, blk.ptr = blk.ptr, 0
@@ -410,12 +439,20 @@ class _PinnedPool:
             if self.cached + blk.cap <= self.LIMIT:
                 self.free.setdefault(blk.cap, []).append(ptr)
                 self.cached += blk.cap
-                return
-        # the block may still be the source of an asynchronous upload
+            else:
+                self.pending.append(ptr)
+
+    def drain(self) -> None:
+        with self.lock:
+            ptrs, self.pending = self.pending, []
+        if not ptrs:
+            return
+        # a block may still be the source of an asynchronous upload
         # (upload_immutable): let every device drain before unpinning it
         for dev in range(device_count()):
             _lib.sf_device_sync(dev)
-        _lib.sf_host_free(ptr)
+        for ptr in ptrs:
+            _lib.sf_host_free(ptr)
 
 
 _PINNED = _PinnedPool()

@@ -604,8 +604,13 @@ def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
     # fast path: the same program as last call when every input is either the
     # very same object (its signature cannot have changed: tensors are
     # immutable, a variable's dtype/shape fixed) or has the same signature
+    rt = get_runtime()
+    opts = rt.options
+    # compiled programs depend on the runtime's RNG mode, fusion switch and
+    # registry: a program from an earlier runtime is never reused
+    pkey = (device, rt.generation, opts.rng, opts.fuse)
     last = gf.__dict__.get("_last_prog")
-    if last is not None and last[0] == device and len(last[1]) == len(inputs):
+    if last is not None and last[0] == pkey and len(last[1]) == len(inputs):
         refs, comps, prog = last[1], last[2], last[3]
         for i, v in enumerate(inputs):
             if refs[i]() is v:
@@ -615,13 +620,14 @@ def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
             refs[i] = weakref.ref(v)
         else:
             return prog
-    key = (device, _signature(inputs))
+    key = (pkey, _signature(inputs))
     prog = cache.get(key)
     if prog is None:
-        opts = get_runtime().options
+        if any(k[0][1] != rt.generation for k in cache):
+            cache.clear()  # programs of a replaced runtime
         prog = Program(gf, inputs, device, libraries, opts.rng, opts.fuse)
         cache[key] = prog
-    gf._last_prog = (device, [weakref.ref(v) for v in inputs], list(key[1]), prog)
+    gf._last_prog = (pkey, [weakref.ref(v) for v in inputs], list(key[1]), prog)
     return prog
 
 

@@ -39,7 +39,7 @@ MIN_BATCH = 2
 # program is cut into chunks of about this many scalar operations; each
 # chunk is its own kernel (rowed values crossing a cut round-trip through
 # L2-resident temporaries) and the chunks compile in parallel.
-# (B200 sweeps, tools/sweep_rows.sh, L2HMC 1e5 chains, before re-rolling:
+# (B200 sweeps, L2HMC 1e5 chains, before re-rolling:
 # 1200 -> 0.38 ms/step, 4800 -> 0.29 ms, 9600 -> 0.28 ms at 3x the compile
 # time, 19200+ slower.  With re-rolled loops the whole transition is ~9000
 # ops: 4800 -> 2 row kernels, 0.202 ms; 9000 -> 1 row kernel, 0.196 ms, and

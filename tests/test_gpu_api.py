@@ -28,24 +28,36 @@ GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
 
 # ---------------------------------------------------------------- tapes
 def test_read_only_pinned_result_uploads_asynchronously():
-    """A result array frozen read-only and fed back (the e2e sampler loop):
-    pooled page-locked memory, uploaded by an asynchronous DMA, doubles as the
-    tensor's host copy; the pool block is reused only by later copies on the
-    same stream, so churning downloads cannot corrupt the upload."""
+    """A result array from Tensor.raw() fed back (the e2e sampler loop):
+    pooled page-locked memory behind a read-only memoryview, uploaded by an
+    asynchronous DMA, doubles as the tensor's host copy; the pool block is
+    reused only by later copies on the same stream, so churning downloads
+    cannot corrupt the upload.  An array the caller froze itself (numpy() +
+    writeable=False) is copied: the caller could unfreeze it."""
     from paper_1903_01855_b200 import _native
 
     n = 300000
     base = np.arange(n, dtype=np.float32)
-    h = sf.constant(base).numpy()
-    h.flags.writeable = False
-    assert _native.pooled_pinned(h)
+    h = sf.constant(base).raw()
+    assert _native.frozen_pinned(h)
+    with pytest.raises(ValueError):
+        h.flags.writeable = True
     t = sf.tensor_from_host(h, (n,), sf.float32)
-    assert t.raw() is not None and not t.raw().flags.writeable
+    assert t.raw() is h
     y = sf.add(t, sf.constant(np.float32(1.0)))
     del h
     for _ in range(5):
         z = y.numpy()
     np.testing.assert_array_equal(z, base + np.float32(1.0))
+    # a caller-frozen array is not trusted: synchronous private copy
+    u = sf.constant(base).numpy()
+    u.flags.writeable = False
+    assert not _native.frozen_pinned(u)
+    t3 = sf.tensor_from_host(u, (n,), sf.float32)
+    assert t3.raw() is not u
+    u.flags.writeable = True
+    u[:] = -1
+    np.testing.assert_array_equal(t3.numpy(), base)
     # writable or user-owned arrays keep the synchronous copy
     w = base.copy()
     t2 = sf.tensor_from_host(w, (n,), sf.float32)
