@@ -205,8 +205,9 @@ class L2HMC:
         v, l4 = self._mom(x, v, t, fwd)
         return x, v, (l1 + l2) + (l3 + l4)
 
-    def _kernel(self, x, fwd):
-        v = self.rt.standard_normal((self.batch, 2)).astype(F32)
+    def _kernel(self, x, fwd, v=None):
+        if v is None:
+            v = self.rt.standard_normal((self.batch, 2)).astype(F32)
         xp, vp, logdet = x, v, None
         for i in range(self.N_STEPS):
             xp, vp, ld = self._lf(xp, vp, i, fwd)
@@ -220,15 +221,26 @@ class L2HMC:
     def transition(self):
         x = self.x
         b = self.batch
-        xf, pf = self._kernel(x, True)
-        xb, pb = self._kernel(x, False)
-        fwd = (self.rt.random((b,)).astype(F32) > F32(0.5)).astype(F32)
+        vf = self.rt.standard_normal((b, 2)).astype(F32)
+        vb = self.rt.standard_normal((b, 2)).astype(F32)
+        u_dir = self.rt.random((b,)).astype(F32)
+        u_acc = self.rt.random((b,)).astype(F32)
+        self.x, acc_prob = self.transition_with(x, vf, vb, u_dir, u_acc)
+        return np.concatenate([self.x.ravel(), acc_prob.ravel()])
+
+    def transition_with(self, x, vf, vb, u_dir, u_acc):
+        """One transition of state x with the four draws given (the
+        ``draws="inputs"`` program); returns (x_out, accept_prob)."""
+        b = x.shape[0]
+        xf, pf = self._kernel(x, True, vf)
+        xb, pb = self._kernel(x, False, vb)
+        fwd = (u_dir > F32(0.5)).astype(F32)
         bwd = F32(1.0) - fwd
         x_post = fwd.reshape(b, 1) * xf + bwd.reshape(b, 1) * xb
         acc_prob = fwd * pf + bwd * pb
-        acc = (acc_prob > self.rt.random((b,)).astype(F32)).astype(F32)
-        self.x = acc.reshape(b, 1) * x_post + (F32(1.0) - acc).reshape(b, 1) * x
-        return np.concatenate([self.x.ravel(), acc_prob.ravel()])
+        acc = (acc_prob > u_acc).astype(F32)
+        x_out = acc.reshape(b, 1) * x_post + (F32(1.0) - acc).reshape(b, 1) * x
+        return x_out, acc_prob
 
 
 # ---------------------------------------------------------------------------

@@ -53,13 +53,28 @@ class _Net:
 
 
 class L2HMCSampler:
-    """apply_transition(x) -> (x_out, accept_prob); staged or eager."""
+    """apply_transition(x) -> (x_out, accept_prob); staged or eager.
+
+    ``draws="runtime"`` (the benchmarked program): the momenta and the two
+    uniforms come from the runtime's random ops inside the transition (device
+    Philox fused into the row kernel, or the host PCG64 stream).
+    ``draws="inputs"``: the same program with the four draws passed in as
+    arguments, ``apply_transition(x, v_fwd, v_bwd, u_dir, u_acc)``; they are
+    drawn on the host from ``default_rng(draw_seed)`` in the reference
+    runtime's order (oracle/workloads_np.py L2HMC) — the staged program is then
+    still one fused row kernel, and comparable with the oracle at any batch.
+    """
 
     gate_tol = 1e-5
 
-    def __init__(self, sf, batch: int, mode: str = "staged", seed: int = 0):
+    def __init__(self, sf, batch: int, mode: str = "staged", seed: int = 0,
+                 draws: str = "runtime", draw_seed: int = 0):
+        if draws not in ("runtime", "inputs"):
+            raise ValueError(f"draws must be 'runtime' or 'inputs', got {draws!r}")
         self.sf = sf
         self.batch = batch
+        self.draws = draws
+        self.draw_rng = np.random.default_rng(draw_seed)
         rng = np.random.default_rng(seed)
         self.position_fn = _Net(sf, rng, 2.0)
         self.momentum_fn = _Net(sf, rng, 1.0)
@@ -171,9 +186,10 @@ class L2HMCSampler:
             v, l4 = self._momentum_bwd(x, v, t)
         return x, v, sf.add(sf.add(l1, l2), sf.add(l3, l4))
 
-    def transition_kernel(self, x, forward):
+    def transition_kernel(self, x, forward, v=None):
         sf = self.sf
-        v = sf.random_normal((self.batch, X_DIM))
+        if v is None:
+            v = sf.random_normal((self.batch, X_DIM))
         x_post, v_post = x, v
         logdet = None
         for i in range(N_STEPS):
@@ -185,26 +201,44 @@ class L2HMCSampler:
         prob = self._op("select", finite, prob, _f32(sf, 0.0))
         return x_post, v_post, prob
 
-    def apply_transition(self, x):
+    def apply_transition(self, x, v_fwd=None, v_bwd=None, u_dir=None, u_acc=None):
         sf = self.sf
         b = self.batch
-        x_f, _v_f, p_f = self.transition_kernel(x, True)
-        x_b, _v_b, p_b = self.transition_kernel(x, False)
-        u_dir = self._op("random_uniform", shape=(b,), dtype=sf.float32)
+        x_f, _v_f, p_f = self.transition_kernel(x, True, v_fwd)
+        x_b, _v_b, p_b = self.transition_kernel(x, False, v_bwd)
+        if u_dir is None:
+            u_dir = self._op("random_uniform", shape=(b,), dtype=sf.float32)
         fwd = self._op("cast", sf.greater(u_dir, 0.5), dtype=sf.float32)
         bwd = sf.sub(1.0, fwd)
         fwd2, bwd2 = sf.reshape(fwd, (b, 1)), sf.reshape(bwd, (b, 1))
         x_post = sf.add(sf.mul(fwd2, x_f), sf.mul(bwd2, x_b))
         accept_prob = sf.add(sf.mul(fwd, p_f), sf.mul(bwd, p_b))
-        u_acc = self._op("random_uniform", shape=(b,), dtype=sf.float32)
+        if u_acc is None:
+            u_acc = self._op("random_uniform", shape=(b,), dtype=sf.float32)
         acc = self._op("cast", sf.greater(accept_prob, u_acc), dtype=sf.float32)
         acc2 = sf.reshape(acc, (b, 1))
         x_out = sf.add(sf.mul(acc2, x_post), sf.mul(sf.reshape(sf.sub(1.0, acc), (b, 1)), x))
         return x_out, accept_prob
 
     # -- harness -------------------------------------------------------------------
-    def step(self):
-        self.x, self.accept = self.transition(self.x)
+    def host_draws(self):
+        """The four draws of one transition, in the reference runtime's
+        order: normal (B,2) forward, normal (B,2) backward, uniform (B,)
+        direction, uniform (B,) accept (f64 draws rounded to f32)."""
+        r, b = self.draw_rng, self.batch
+        return (r.standard_normal((b, X_DIM)).astype(np.float32),
+                r.standard_normal((b, X_DIM)).astype(np.float32),
+                r.random((b,)).astype(np.float32), r.random((b,)).astype(np.float32))
+
+    def step(self, draws=None):
+        if self.draws == "inputs":
+            if draws is None:
+                draws = self.host_draws()
+            ts = [self.sf.tensor_from_host(d.reshape(-1), d.shape, self.sf.float32)
+                  for d in draws]
+            self.x, self.accept = self.transition(self.x, *ts)
+        else:
+            self.x, self.accept = self.transition(self.x)
         return self.x
 
     def run_iteration(self):

@@ -56,3 +56,54 @@ def test_l2hmc_oracle(b):
     m = workloads_np.L2HMC(b, seed=0, runtime_seed=0)
     got = np.stack([m.transition() for _ in range(3)])
     np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-6)
+
+
+# ---------------------------------------------------------------- device RNG oracle
+def test_philox_oracle_known_answers():
+    """oracle/philox_np.py reproduces the published Random123 philox4x32_10
+    known-answer vectors (the device generator is pinned to this oracle in
+    tests/test_gpu_rng.py)."""
+    from oracle import philox_np
+
+    for ctr, key, want in philox_np.KAT:
+        got = philox_np.philox4x32_10(*ctr, *key)
+        assert [int(w) for w in got] == list(want)
+
+
+def test_philox_oracle_draw_mapping():
+    from oracle import philox_np
+
+    u = philox_np.uniform_f32(4, seed=0, offset=0)
+    assert u[0] == np.float32((0x6627E8D5 >> 8) * 2.0 ** -24)
+    assert u.dtype == np.float32 and np.all((u >= 0) & (u < 1))
+    z = philox_np.normal_f64(200000, seed=5, offset=7)
+    assert abs(z.mean()) < 0.02 and abs(z.var() - 1) < 0.02
+    # offset shifts the stream: element i of (offset k) == element i+k of (offset 0)
+    a = philox_np.uniform_f64(10, seed=9, offset=3)
+    b = philox_np.uniform_f64(13, seed=9, offset=0)
+    assert a.tobytes() == b[3:].tobytes()
+
+
+# ---------------------------------------------------------------- L2HMC at the headline batch
+GOLD2 = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_r2.npz"))
+
+
+def test_l2hmc_oracle_matches_reference_at_1e5():
+    """The oracle (draws passed in) against the reference run at 1e5 chains
+    (tests/golden/make_golden_r2.py): first 4096 chains of each of three
+    transitions, and float64 sums over all chains."""
+    b = 100_000
+    m = workloads_np.L2HMC(b, seed=0)
+    rng = np.random.default_rng(0)
+    for t in (1, 2, 3):
+        draws = (rng.standard_normal((b, 2)).astype(np.float32),
+                 rng.standard_normal((b, 2)).astype(np.float32),
+                 rng.random((b,)).astype(np.float32), rng.random((b,)).astype(np.float32))
+        m.x, acc = m.transition_with(m.x, *draws)
+        np.testing.assert_allclose(m.x[:4096], GOLD2[f"l2hmc_inputs_1e5_t{t}_x_head"],
+                                   rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(acc[:4096], GOLD2[f"l2hmc_inputs_1e5_t{t}_acc_head"],
+                                   rtol=1e-5, atol=1e-6)
+        x64, a64 = m.x.astype(np.float64), acc.astype(np.float64)
+        np.testing.assert_allclose([np.square(x64).sum(), a64.sum()],
+                                   GOLD2[f"l2hmc_inputs_1e5_t{t}_sums"][[1, 2]], rtol=1e-5)
