@@ -375,4 +375,34 @@ SF_DEVFN double2 ldp2(unsigned b) {
   return v;
 }
 
+// Packed fp32 pairs (sm_100a FADD2 / FMUL2 / FFMA2): two independent IEEE
+// round-to-nearest operations in one instruction, bit-identical to the
+// scalar add / sub / mul / __fmaf_rn on each half (denormals kept).
+// CAUTION: ptxas contracts mul2 followed by add2/sub2 into FFMA2 even under
+// -fmad=false; generated code never feeds mul2 into an add (rowfuse.PACK).  Row programs keep adjacent elements of a chain's row in a float2;
+// a scalar operand broadcast to both halves (make_float2(s, s)) becomes the
+// instruction's .F32 operand form, not a register copy.
+SF_DEVFN unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+SF_DEVFN float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+SF_DEVFN float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+SF_DEVFN float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+SF_DEVFN float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+SF_DEVFN float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(r);
+}
+
 }  // namespace sf

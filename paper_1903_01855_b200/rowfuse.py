@@ -65,6 +65,15 @@ REPLICA_MIN_BATCH = 1 << 62
 SM_COUNT = 148
 # matvec weight vectors loaded ahead of their FMAs (latency hiding vs registers)
 PREFETCH = int(__import__("os").environ.get("SF_PREFETCH", "4"))
+# adjacent fp32 row elements computed as packed pairs (sm_100a FADD2 /
+# FFMA2: one instruction for two IEEE operations, bit-identical to the
+# scalar ones) in elementwise add/sub and in matvec accumulators.
+# Multiplies stay scalar: ptxas (12.9) contracts mul.rn.f32x2 + add.rn.f32x2
+# into FFMA2 even under -fmad=false (measured: the fused leapfrog then
+# differed from eager in 77% of elements), while a scalar FMUL feeding an
+# FADD2 is never fused.
+PACK = __import__("os").environ.get("SF_ROW_PACK", "1") == "1"
+_PACKED = {"add": "sf::add2", "sub": "sf::sub2"}
 # re-roll repeated blocks of row ops into loops (LoopOp)
 REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
@@ -586,6 +595,7 @@ class _Gen:
         self.level: Dict[int, int] = {}
         self.uni_ops: List[Tuple[int, int, str]] = []  # (level, work, code)
         self.block = 128
+        self.f2vars: set = set()  # names declared float2 (packed row pairs)
         # chains per thread: replica k owns row r + 128 k of the CTA's 128 R
         # rows; the replicas' statements are emitted interleaved, op by op,
         # so they share every weight load and double the ILP
@@ -1025,6 +1035,20 @@ class _Gen:
             out[q] = elems
         return out
 
+    def _pair(self, e0: str, e1: str, lines: List[str]) -> str:
+        """float2 operand from two element expressions: a packed variable's
+        own pair, a scalar broadcast, or a fresh make_float2."""
+        if e0.endswith(".x") and e1.endswith(".y") and e0[:-2] == e1[:-2] \
+                and e0[:-2] in self.f2vars:
+            return e0[:-2]
+        if e0 == e1:
+            if "(" in e0 and not e0.startswith("__int_as_float("):
+                t = self._new_tmp()  # a shared-memory load: issue it once
+                lines.append(f"const float {t} = {e0};")
+                e0 = t
+            return f"make_float2({e0}, {e0})"
+        return f"make_float2({e0}, {e1})"
+
     def _emit_rowed(self, op: LOp, L) -> None:
         _, w, rank = L
         o = op.outs[0]
@@ -1034,7 +1058,26 @@ class _Gen:
         self.rowed_names[id(o)] = per_rep
         lines = []
         k = op.kind
-        if k == "ew":
+        if k == "ew" and PACK and op.name in _PACKED and o.dtype is DType.float32 and w >= 2:
+            vec = self._vector_operands(op, w, lines)
+            fn = _PACKED[op.name]
+            for rep in range(self.R):
+                self.rep = rep
+                names = per_rep[rep]
+                for j in range(w):
+                    args = [vec[q][j] if q in vec else self.row_elem(x, j, w, rank)
+                            for q, x in enumerate(op.ins)]
+                    if j % 2 == 0 and j + 1 < w:
+                        args1 = [vec[q][j + 1] if q in vec else self.row_elem(x, j + 1, w, rank)
+                                 for q, x in enumerate(op.ins)]
+                        pn = f"{base}_p{j // 2}{self.sfx(rep)}"
+                        ops2 = [self._pair(a0, a1, lines) for a0, a1 in zip(args, args1)]
+                        lines.append(f"const float2 {pn} = {fn}({ops2[0]}, {ops2[1]});")
+                        self.f2vars.add(pn)
+                        names[j], names[j + 1] = pn + ".x", pn + ".y"
+                    elif j % 2 == 0:
+                        lines.append(f"const {ct} {names[j]} = {ew_expr(op.name, args, ct)};")
+        elif k == "ew":
             vec = self._vector_operands(op, w, lines)
             for j in range(w):
                 for rep in range(self.R):
@@ -1065,8 +1108,24 @@ class _Gen:
                 vw = 16 // br.dtype.width
                 vt = "float4" if vw == 4 else "double2"
                 comp = "xyzw"
-                lines.append(" ".join(f"{ct} {nm} = ({ct})0;" for names in per_rep
-                                      for nm in names))
+                # packed accumulators: output pairs (c, c + 1) whose weights
+                # sit in one vector's .xy or .zw for every k
+                pk = (PACK and o.dtype is DType.float32 and
+                      all(((kk * Np + c) % vw) % 2 == 0 for kk in range(kk_n)
+                          for c in range(0, n - 1, 2)))
+                npair = n // 2 if pk else 0
+                for rep in range(self.R):
+                    names = per_rep[rep]
+                    decl = []
+                    for c in range(n):
+                        if c < 2 * npair:
+                            if c % 2 == 0:
+                                pn = f"{base}_p{c // 2}{self.sfx(rep)}"
+                                self.f2vars.add(pn)
+                                decl.append(f"float2 {pn} = make_float2(0.0f, 0.0f);")
+                        else:
+                            decl.append(f"{ct} {names[c]} = ({ct})0;")
+                    lines.append(" ".join(decl))
                 # weight vectors in first-use order, issued PREFETCH vectors
                 # ahead of the FMAs that consume them (volatile loads keep
                 # program order, so this is the issue order)
@@ -1095,11 +1154,24 @@ class _Gen:
                         f = kk * Np + c
                         v = f // vw
                         issue_upto(order.index(v) + 1 + PREFETCH, stmt)
+                        if c < 2 * npair:
+                            if c % 2:
+                                continue
+                            for rep in range(self.R):
+                                pn = f"{base}_p{c // 2}{self.sfx(rep)}"
+                                x = xs_rep[rep][kk]
+                                stmt.append(f"{pn} = sf::fma2(make_float2({x}, {x}), make_float2("
+                                            f"{vecs[v]}.{comp[f % vw]}, {vecs[v]}.{comp[f % vw + 1]}"
+                                            f"), {pn});")
+                            continue
                         for rep in range(self.R):
                             nm = per_rep[rep][c]
                             stmt.append(f"{nm} = {fma}({xs_rep[rep][kk]}, "
                                         f"{vecs[v]}.{comp[f % vw]}, {nm});")
                     lines.append(" ".join(stmt))
+                for rep in range(self.R):
+                    for c in range(2 * npair):
+                        per_rep[rep][c] = f"{base}_p{c // 2}{self.sfx(rep)}.{'xy'[c % 2]}"
             else:
                 for j in range(n):
                     for rep in range(self.R):
