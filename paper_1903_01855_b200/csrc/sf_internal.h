@@ -37,6 +37,7 @@ struct DriverApi {
   CUresult (*getErrorString)(CUresult, const char**) = nullptr;
   CUresult (*moduleLoadData)(CUmodule*, const void*) = nullptr;
   CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*moduleGetGlobal)(CUdeviceptr*, size_t*, CUmodule, const char*) = nullptr;
   CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, unsigned, CUstream, void**, void**) = nullptr;
@@ -152,5 +153,18 @@ int launch_rng(Device* d, int kind, int dtype, int64_t n, unsigned long long see
 int launch_dropout(Device* d, int dtype, int64_t n, const void* x, const void* u,
                    int u_dtype, double rate, void* out, void* mask);
 int launch_cast(Device* d, int src_dtype, int dst_dtype, int64_t n, const void* in, void* out);
+
+// Row-kernel constant pool (sf_plan.cpp step kind 1 with a pool section):
+// gather the kernel's uniform operands into `image` at their pool offsets
+// (rows of N elements padded to Np), then the image is copied into the
+// module's __constant__ cpool.
+struct CpoolEntry {
+  const void* src;
+  uint32_t dst_off, n, width, N, Np, pad;
+};
+int launch_cpool_gather(Device* d, const CpoolEntry* e, int n, void* image);
+// device address and size of a jitted kernel's module global (loads the module)
+int jit_global(void* kernel, int dev, const char* name, void** ptr, size_t* bytes);
+std::mutex& jit_mutex(void* kernel);
 
 }  // namespace sfrt

@@ -22,6 +22,7 @@ struct JitKernel {
   std::string name;
   std::vector<char> cubin;
   std::mutex mu;
+  std::mutex pool_mu;  // constant-pool fill + launch are one unit per module
   CUmodule module[64] = {};
   CUfunction fn[64] = {};
 };
@@ -162,6 +163,20 @@ int jit_function(JitKernel* k, int dev, CUfunction* out) {
   *out = k->fn[dev];
   return SF_OK;
 }
+
+int jit_global(void* kernel, int dev, const char* name, void** ptr, size_t* bytes) {
+  JitKernel* k = (JitKernel*)kernel;
+  CUfunction f;
+  SF_TRY(jit_function(k, dev, &f));  // loads the module on this device
+  CUdeviceptr p = 0;
+  size_t n = 0;
+  SF_CHECK_CU(drv.moduleGetGlobal(&p, &n, k->module[dev], name));
+  *ptr = (void*)p;
+  *bytes = n;
+  return SF_OK;
+}
+
+std::mutex& jit_mutex(void* kernel) { return ((JitKernel*)kernel)->pool_mu; }
 
 int jit_launch(Device* d, void* kernel, unsigned grid, unsigned block, unsigned smem,
                const void* params, size_t params_bytes) {

@@ -3,6 +3,9 @@
 // Reference kernels: _transpose_kernel (kernels.py:211-219), _eye_kernel
 // (:282-292), _random_normal_kernel (:372-384), _dropout_kernel (:387-404),
 // zeros_for/ones_for (gradients.py:65-76).
+#include <cstring>
+#include <mutex>
+
 #include "sf_internal.h"
 #include "sf_ops.cuh"
 
@@ -162,6 +165,43 @@ int launch_dropout(Device* d, int dtype, int64_t n, const void* x, const void* u
     return SF_ERR_INVALID;
   }
   SF_CHECK_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+
+// Constant-pool gather: one CTA per entry copies a uniform operand into the
+// pool image at its offset (row q / N of the operand lands at row stride Np).
+static constexpr int CPOOL_BATCH = 960;  // entries per launch (kernel params <= 32 KB)
+struct CpoolParams {
+  unsigned char* image;
+  int n;
+  CpoolEntry e[CPOOL_BATCH];
+};
+
+__global__ void cpool_gather_kernel(const __grid_constant__ CpoolParams p) {
+  const CpoolEntry& e = p.e[blockIdx.x];
+  unsigned char* dst = p.image + e.dst_off;
+  for (unsigned q = threadIdx.x; q < e.n; q += blockDim.x) {
+    const unsigned o = ((q / e.N) * e.Np + q % e.N) * e.width;
+    if (e.width == 4) *(uint32_t*)(dst + o) = ((const uint32_t*)e.src)[q];
+    else if (e.width == 8) *(uint64_t*)(dst + o) = ((const uint64_t*)e.src)[q];
+    else dst[o] = ((const unsigned char*)e.src)[q];
+  }
+}
+
+int launch_cpool_gather(Device* d, const CpoolEntry* e, int n, void* image) {
+  static CpoolParams p;  // large: not on the stack (callers hold the module's pool lock)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int b = 0; b < n; b += CPOOL_BATCH) {
+    const int m = n - b < CPOOL_BATCH ? n - b : CPOOL_BATCH;
+    p.image = (unsigned char*)image;
+    p.n = m;
+    std::memcpy(p.e, e + b, sizeof(CpoolEntry) * (size_t)m);
+    count_launch(d->id);
+    cpool_gather_kernel<<<m, 128, 0, d->stream>>>(p);
+    SF_CHECK_CUDA(cudaGetLastError());
+  }
   return SF_OK;
 }
 

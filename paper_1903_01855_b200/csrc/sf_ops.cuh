@@ -405,4 +405,84 @@ SF_DEVFN float2 fma2(float2 a, float2 b, float2 c) {
   return u2f(r);
 }
 
+// Row-kernel constant pool (rowfuse.CONST_POOL): a generated row kernel
+// declares `__constant__ unsigned char cpool[]` holding its uniform operands
+// (weights, biases, per-step stacked uniforms); the plan gathers them there
+// before each launch (sf_plan.cpp).  Warp-uniform loads from the constant
+// bank become uniform-datapath loads (LDCU) feeding FFMA/FFMA2 through
+// uniform-register operands: no per-thread LSU traffic, no shared-memory
+// staging prologue.  The loads are volatile asm (kept in program order:
+// NVVM otherwise schedules them early and pins hundreds of weights in
+// registers, 4.7 KB of spills measured); `dep` (the loop counter inside
+// re-rolled loops) and `SITE` (unique per use) make every use distinct.
+#ifdef SF_CPOOL
+#define SF_CL(NAME, T, PTX, CON)                                                    \
+  template <int OFF, int SITE>                                                      \
+  SF_DEVFN T NAME(int dep) {                                                        \
+    T v;                                                                            \
+    asm volatile("ld.const." PTX " %0, [cpool+%1];" : "=" CON(v) : "n"(OFF), "r"(dep), "n"(SITE)); \
+    return v;                                                                       \
+  }                                                                                 \
+  template <int OFF, int SITE>                                                      \
+  SF_DEVFN T NAME##s(int stride) {                                                  \
+    T v;                                                                            \
+    unsigned long long b;                                                           \
+    asm("mov.u64 %0, cpool;" : "=l"(b));                                            \
+    asm volatile("ld.const." PTX " %0, [%1+%2];" : "=" CON(v) : "l"(b + (unsigned long long)stride), \
+        "n"(OFF), "n"(SITE));                                                       \
+    return v;                                                                       \
+  }
+SF_CL(clf, float, "f32", "f")
+SF_CL(cld, double, "f64", "d")
+SF_CL(cli, int, "s32", "r")
+#undef SF_CL
+template <int OFF, int SITE>
+SF_DEVFN bool clb(int dep) {
+  unsigned short v;
+  asm volatile("ld.const.u8 %0, [cpool+%1];" : "=h"(v) : "n"(OFF), "r"(dep), "n"(SITE));
+  return v != 0;
+}
+template <int OFF, int SITE>
+SF_DEVFN bool clbs(int stride) {
+  unsigned short v;
+  unsigned long long b;
+  asm("mov.u64 %0, cpool;" : "=l"(b));
+  asm volatile("ld.const.u8 %0, [%1+%2];" : "=h"(v) : "l"(b + (unsigned long long)stride), "n"(OFF),
+      "n"(SITE));
+  return v != 0;
+}
+template <int OFF, int SITE>
+SF_DEVFN float4 clf4(int dep) {
+  float4 v;
+  asm volatile("ld.const.v4.f32 {%0, %1, %2, %3}, [cpool+%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "n"(OFF), "r"(dep), "n"(SITE));
+  return v;
+}
+template <int OFF, int SITE>
+SF_DEVFN float4 clf4s(int stride) {
+  float4 v;
+  unsigned long long b;
+  asm("mov.u64 %0, cpool;" : "=l"(b));
+  asm volatile("ld.const.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(b + (unsigned long long)stride), "n"(OFF), "n"(SITE));
+  return v;
+}
+template <int OFF, int SITE>
+SF_DEVFN double2 cld2(int dep) {
+  double2 v;
+  asm volatile("ld.const.v2.f64 {%0, %1}, [cpool+%2];" : "=d"(v.x), "=d"(v.y) : "n"(OFF), "r"(dep), "n"(SITE));
+  return v;
+}
+template <int OFF, int SITE>
+SF_DEVFN double2 cld2s(int stride) {
+  double2 v;
+  unsigned long long b;
+  asm("mov.u64 %0, cpool;" : "=l"(b));
+  asm volatile("ld.const.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y)
+      : "l"(b + (unsigned long long)stride), "n"(OFF), "n"(SITE));
+  return v;
+}
+#endif  // SF_CPOOL
+
 }  // namespace sf

@@ -19,6 +19,11 @@
 //   n_steps x step:  u32 kind | u32 payload_bytes | payload
 //     kind 1 JIT       u64 kernel | u32 grid | u32 block | u32 smem | u32 n_ptr |
 //                      i32 slot[n_ptr] | u32 n_scalar_bytes | bytes (8-aligned)
+//                      [| u32 n_patches | {u32 kind, u32 offset, u64 count}[n]
+//                      [| u32 pool_bytes | u32 n_pool |
+//                         {i32 slot, u32 off, u32 n, u32 width, u32 N, u32 Np}[n]]]
+//                      (pool: the kernel's __constant__ cpool is filled from
+//                      the slots before every launch)
 //     kind 2 MATMUL    i32 dtype | i32 ta | i32 tb | i32 a | i32 b | i32 c | i64 m | i64 n | i64 k
 //     kind 3 REDUCE    i32 op | i32 dtype | i32 ndim | u32 axes | i32 in | i32 out | i64 shape[8]
 //     kind 4 TRANSPOSE i32 dtype | i32 in | i32 out | i32 pad | i64 rows | i64 cols
@@ -60,6 +65,10 @@ struct Step {
     uint64_t count;
   };
   std::vector<Patch> patches;
+  // constant pool of a row kernel: bytes, entries (src = slot index)
+  uint32_t pool_bytes = 0;
+  std::vector<CpoolEntry> pool;
+  std::vector<int32_t> pool_slots;
   std::vector<int32_t> frees;  // temp slots to release after this step
   std::vector<int32_t> defs;   // temp/output slots to allocate before this step
 };
@@ -137,6 +146,33 @@ static int run_step(Plan* p, Device* d, Step& s, std::vector<void*>& ptr) {
           std::memcpy(blob.data() + s.ptr_slots.size() * 8 + pt.offset, &v, 8);
         }
       }
+      if (!s.pool_bytes)
+        return jit_launch(d, s.kernel, s.grid, s.block, s.smem, blob.data(), blob.size());
+      // gather the uniform operands into an image, copy it into the
+      // module's __constant__ pool, launch; one unit per module (stream order)
+      void* cpool = nullptr;
+      size_t cbytes = 0;
+      SF_TRY(jit_global(s.kernel, d->id, "cpool", &cpool, &cbytes));
+      if (cbytes < s.pool_bytes) {
+        set_error("plan: constant pool smaller than its image");
+        return SF_ERR_INVALID;
+      }
+      std::vector<CpoolEntry> ents(s.pool);
+      for (size_t i = 0; i < ents.size(); ++i) ents[i].src = P(s.pool_slots[i]);
+      std::lock_guard<std::mutex> lk(jit_mutex(s.kernel));
+      void* image = nullptr;
+      SF_TRY(d->alloc.alloc(d->id, s.pool_bytes, &image));
+      int rc = launch_cpool_gather(d, ents.data(), (int)ents.size(), image);
+      if (rc == SF_OK) {
+        cudaError_t e = cudaMemcpyAsync(cpool, image, s.pool_bytes, cudaMemcpyDeviceToDevice,
+                                        d->stream);
+        if (e != cudaSuccess) {
+          set_error(std::string("plan: constant pool copy: ") + cudaGetErrorString(e));
+          rc = SF_ERR_CUDA;
+        }
+      }
+      d->alloc.release(image);  // stream-ordered reuse
+      if (rc != SF_OK) return rc;
       return jit_launch(d, s.kernel, s.grid, s.block, s.smem, blob.data(), blob.size());
     }
     case 2:
@@ -270,8 +306,28 @@ int sf_plan_create(int dev, const void* desc, size_t desc_bytes, void** out) {
           s.patches.push_back(pt);
         }
       }
+      if (off + 8 <= b.size()) {  // constant pool section
+        s.pool_bytes = at<uint32_t>(b, off);
+        const uint32_t ne = at<uint32_t>(b, off + 4);
+        off += 8;
+        for (uint32_t k = 0; k < ne; ++k, off += 24) {
+          if (off + 24 > b.size()) return bad("jit pool");
+          CpoolEntry e{};
+          s.pool_slots.push_back(at<int32_t>(b, off));
+          e.dst_off = at<uint32_t>(b, off + 4);
+          e.n = at<uint32_t>(b, off + 8);
+          e.width = at<uint32_t>(b, off + 12);
+          e.N = at<uint32_t>(b, off + 16);
+          e.Np = at<uint32_t>(b, off + 20);
+          if (e.N == 0 || e.Np < e.N || (uint64_t)e.dst_off + (uint64_t)e.Np * e.width *
+              ((e.n + e.N - 1) / e.N) > s.pool_bytes)
+            return bad("jit pool entry");
+          s.pool.push_back(e);
+        }
+      }
     }
     if (s.kind != 7) ++p->n_launches;
+    if (s.kind == 1 && s.pool_bytes) p->n_launches += (int)((s.pool.size() + 959) / 960);
   }
   for (int i = 0; i < n_slots; ++i) {
     const Slot& s = p->slots[i];

@@ -230,6 +230,7 @@ int sf_init(int* n_devices) {
   SF_TRY(resolve("cuGetErrorString", &drv.getErrorString));
   SF_TRY(resolve("cuModuleLoadData", &drv.moduleLoadData));
   SF_TRY(resolve("cuModuleGetFunction", &drv.moduleGetFunction));
+  SF_TRY(resolve("cuModuleGetGlobal", &drv.moduleGetGlobal));
   SF_TRY(resolve("cuFuncSetAttribute", &drv.funcSetAttribute));
   SF_TRY(resolve("cuLaunchKernel", &drv.launchKernel));
   SF_TRY(resolve("cuTensorMapEncodeTiled", &drv.tensorMapEncodeTiled));

@@ -340,8 +340,14 @@ class Program:
         payload += struct.pack("<I", len(patches))
         for kind, off, count in patches:
             payload += struct.pack("<IIQ", kind, off, count)
+        if rp.cpool:
+            # uniform operands gathered into the kernel's __constant__ pool
+            pool_bytes, entries = rp.cpool
+            payload += struct.pack("<II", pool_bytes, len(entries))
+            for k, off, n, width, N, Np in entries:
+                payload += struct.pack("<iIIIII", in_slots[k], off, n, width, N, Np)
         pw.step(1, payload, defs=out_slots, uses=in_slots)
-        return 1
+        return 1 + (-(-len(rp.cpool[1]) // 960) if rp.cpool else 0)
 
     def _emit_single_ew(self, pw, op: LOp, use, define) -> int:
         o = op.outs[0]

@@ -20,6 +20,7 @@ index) as sf_misc.cu.
 from __future__ import annotations
 
 import hashlib
+import re
 from typing import Dict, List, Optional, Tuple
 
 from . import dtypes
@@ -59,6 +60,9 @@ MIN_BLOCKS = int(__import__("os").environ.get("SF_MIN_BLOCKS", "0"))
 # refetch): with the L2 flushed between steps, as bench.py times the
 # headline, 0.204 -> 0.239 ms.  Automatic keeps 1 chain per thread; set
 # SF_ROW_REPLICAS=2 (or REPLICA_MIN_BATCH) for warm-cache serving loops.
+# Round 2: with two chains per thread, element j of both chains shares one
+# float2 (FADD2 / FFMA2 with the weight broadcast, "xpack"); still slower on
+# the flushed headline step (0.171 -> 0.192 ms, 168 registers, 10.6 warps/SM).
 ROW_REPLICAS = int(__import__("os").environ.get("SF_ROW_REPLICAS", "0"))
 REPLICA_MIN_BATCH = 1 << 62
 # SMs of the target GPU (B200: 148); set by the executor from the device
@@ -74,18 +78,36 @@ PREFETCH = int(__import__("os").environ.get("SF_PREFETCH", "4"))
 # FADD2 is never fused.
 PACK = __import__("os").environ.get("SF_ROW_PACK", "1") == "1"
 _PACKED = {"add": "sf::add2", "sub": "sf::sub2"}
+# Option: row kernels read their uniform operands (weights, biases, stacked
+# per-step uniforms) from a per-module __constant__ pool that the plan
+# gathers before each launch, instead of staging them into shared memory in
+# every CTA.  Warp-uniform constant loads run on the uniform datapath (LDCU)
+# and feed FFMA/FFMA2 as uniform-register operands.  A B200 microbenchmark
+# (10x10 relu matvecs per thread, 1.6 KB of weights) ran 94.5 -> 49.8 us;
+# but ptxas merges repeated constant loads of one address into long-lived
+# registers (4.7 KB of spills), so every use site needs its own copy, and
+# the L2HMC transition's 31 KB pool then runs SLOWER than shared memory
+# (B200: 64 -> 86 us at 200 chains, 166 -> 176 us at 1e5; ncu: the LDCU
+# latency moves the short_scoreboard stall onto the FFMA2s).  Off by
+# default; SF_ROW_CONST=1 enables it (tests keep it bit-exact).
+CONST_POOL = __import__("os").environ.get("SF_ROW_CONST", "0") == "1"
+_CL = {"float": "clf", "double": "cld", "int": "cli", "bool": "clb"}
+CPOOL_BYTES = 60 * 1024  # constant bank 3 holds 64 KB
 # re-roll repeated blocks of row ops into loops (LoopOp)
 REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 
 class RowProgram:
-    __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas")
+    __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas", "cpool")
 
     def __init__(self, batch: int):
         self.ops: List[LOp] = []
         self.batch = batch
         self.gen = None  # cached generate_rowprog result
         self.uniform_only = False  # single-CTA kernel for chain-independent ops
+        # (pool bytes, [(pointer slot, offset, elements, width, N, Np)]) of a
+        # row kernel reading its uniforms from the __constant__ pool
+        self.cpool = None
         self.block = 128  # threads per CTA (set by code generation)
         # chains per thread: large batches take 2 (shared weight loads, 2x ILP)
         self.replicas = ROW_REPLICAS if ROW_REPLICAS else (2 if batch >= REPLICA_MIN_BATCH else 1)
@@ -596,6 +618,11 @@ class _Gen:
         self.uni_ops: List[Tuple[int, int, str]] = []  # (level, work, code)
         self.block = 128
         self.f2vars: set = set()  # names declared float2 (packed row pairs)
+        self.cpool = CONST_POOL and not rp.uniform_only
+        self.cp_entries: List[Tuple[int, int, int, int, int, int]] = []
+        self.cp_arrays: Dict[str, tuple] = {}
+        self.cp_first: Dict[str, int] = {}
+        self.in_loop = False
         # chains per thread: replica k owns row r + 128 k of the CTA's 128 R
         # rows; the replicas' statements are emitted interleaved, op by op,
         # so they share every weight load and double the ILP
@@ -709,6 +736,13 @@ class _Gen:
         if width in (4, 8):
             vw = 16 // width  # slices start 16-byte aligned; vector reads stay inside
             size = -(-size // vw) * vw
+        if self.cpool:
+            # placed per use site by _fill (each op reading the array gets
+            # its own copy, so no two loads share an address)
+            N, Np = self.pad.get(id(r), (max(1, n), max(1, n)))
+            self.pool[name] = (f"@P{name}@", size, ct, width)
+            self.cp_arrays[name] = (list(slots), n, width, N, Np, size)
+            return pidx, size
         # one pool per kernel: every array is a fixed byte offset from one base
         # register, so each load is LDS [base + immediate]
         pos = -(-self.pool_size // 16) * 16
@@ -726,17 +760,60 @@ class _Gen:
 
     def _lds(self, name: str, index: int, stacked: bool) -> str:
         """Scalar load of element ``index`` of pool array ``name`` (of the
-        current loop iteration's slice when stacked)."""
+        current loop iteration's slice when stacked).  Constant-pool loads
+        carry @DEP@ / @SITE@ placeholders, filled per use (_fill)."""
         pos, size, ct, width = self.pool[name]
+        if self.cpool:
+            fn = "sf::" + _CL[ct]
+            if stacked:
+                return f"{fn}s<{pos} + {index * width}, @SITE@>(it * {size * width})"
+            return f"{fn}<{pos} + {index * width}, @SITE@>(@DEP@)"
         base = f"(sp + it * {size * width})" if stacked else "sp"
         return f"sf::ldp<{ct}, {pos + index * width}>({base})"
 
     def _lds_vec(self, name: str, index: int, stacked: bool) -> str:
         """16-byte vector load starting at element ``index`` (aligned)."""
         pos, size, ct, width = self.pool[name]
+        if self.cpool:
+            fn = "sf::clf4" if width == 4 else "sf::cld2"
+            if stacked:
+                return f"{fn}s<{pos} + {index * width}, @SITE@>(it * {size * width})"
+            return f"{fn}<{pos} + {index * width}, @SITE@>(@DEP@)"
         base = f"(sp + it * {size * width})" if stacked else "sp"
         fn = "sf::ldp4" if width == 4 else "sf::ldp2"
         return f"{fn}<{pos + index * width}>({base})"
+
+    def _place(self, name: str) -> int:
+        """A fresh copy of pool array ``name`` for one use site; the plan
+        gathers every copy before the launch.  Past CPOOL_BYTES the first
+        copy is shared."""
+        slots, n, width, N, Np, size = self.cp_arrays[name]
+        nbytes = max(1, size * len(slots)) * width
+        first = self.cp_first.get(name)
+        if first is not None and self.pool_size + nbytes > CPOOL_BYTES:
+            return first
+        pos = -(-self.pool_size // 16) * 16
+        self.pool_size = pos + nbytes
+        for i, k in enumerate(slots):
+            self.cp_entries.append((k, pos + i * size * width, n, width, N, Np))
+        self.cp_first.setdefault(name, pos)
+        return pos
+
+    def _fill(self, line: str) -> str:
+        """Constant-pool load placeholders: the loop counter as the dependency
+        inside re-rolled loops (no hoisting), a unique site id per use (no
+        merging of repeated loads into long-lived registers)."""
+        if "@" not in line:
+            return line
+        line = line.replace("@DEP@", "it" if self.in_loop else "0")
+        for name in dict.fromkeys(re.findall(r"@P(\w+)@", line)):
+            line = line.replace(f"@P{name}@", str(self._place(name)))
+
+        def site(_m):
+            self.tmp += 1
+            return str(self.tmp)
+
+        return re.sub("@SITE@", site, line)
 
     def _ext_slot(self, r: LV, kind: str) -> int:
         """Pointer slot of an external root without staging it."""
@@ -966,9 +1043,11 @@ class _Gen:
             pre.append(" ".join(f"{ct} {nm} = ({ct})0;" for names in per_rep for nm in names))
             exp_names.append(per_rep)
         pre.append(f"#pragma unroll 1\n    for (int it = 0; it < {lp.m}; ++it) {{")
-        self.body.append("    " + "\n    ".join(pre))
+        self.body.append(self._fill("    " + "\n    ".join(pre)))
+        self.in_loop = True
         for op in lp.body:
             self._emit_rowed(op, self.P.layout_of(op.outs[0]))
+        self.in_loop = False
         post = []
         for (e, b), per_rep in zip(lp.exports, exp_names):
             for names, src in zip(per_rep, self.rowed_names[id(b)]):
@@ -1058,7 +1137,23 @@ class _Gen:
         self.rowed_names[id(o)] = per_rep
         lines = []
         k = op.kind
-        if k == "ew" and PACK and op.name in _PACKED and o.dtype is DType.float32 and w >= 2:
+        xpack = PACK and self.R == 2 and o.dtype is DType.float32
+        if k == "ew" and xpack and op.name in _PACKED:
+            # two chains per thread: element j of both chains in one float2
+            vec = self._vector_operands(op, w, lines)
+            fn = _PACKED[op.name]
+            for j in range(w):
+                args = []
+                for rep in range(2):
+                    self.rep = rep
+                    args.append([vec[q][j] if q in vec else self.row_elem(x, j, w, rank)
+                                 for q, x in enumerate(op.ins)])
+                pn = f"{base}_{j}x"
+                ops2 = [self._pair(a0, a1, lines) for a0, a1 in zip(args[0], args[1])]
+                lines.append(f"const float2 {pn} = {fn}({ops2[0]}, {ops2[1]});")
+                self.f2vars.add(pn)
+                per_rep[0][j], per_rep[1][j] = pn + ".x", pn + ".y"
+        elif k == "ew" and PACK and op.name in _PACKED and o.dtype is DType.float32 and w >= 2:
             vec = self._vector_operands(op, w, lines)
             fn = _PACKED[op.name]
             for rep in range(self.R):
@@ -1110,11 +1205,17 @@ class _Gen:
                 comp = "xyzw"
                 # packed accumulators: output pairs (c, c + 1) whose weights
                 # sit in one vector's .xy or .zw for every k
-                pk = (PACK and o.dtype is DType.float32 and
+                pk = (PACK and o.dtype is DType.float32 and not xpack and
                       all(((kk * Np + c) % vw) % 2 == 0 for kk in range(kk_n)
                           for c in range(0, n - 1, 2)))
                 npair = n // 2 if pk else 0
-                for rep in range(self.R):
+                if xpack:
+                    # two chains per thread: output c of both chains in one
+                    # float2, the weight broadcast to both halves
+                    lines.append(" ".join(f"float2 {base}_{c}x = make_float2(0.0f, 0.0f);"
+                                          for c in range(n)))
+                    self.f2vars.update(f"{base}_{c}x" for c in range(n))
+                for rep in range(self.R if not xpack else 0):
                     names = per_rep[rep]
                     decl = []
                     for c in range(n):
@@ -1154,6 +1255,12 @@ class _Gen:
                         f = kk * Np + c
                         v = f // vw
                         issue_upto(order.index(v) + 1 + PREFETCH, stmt)
+                        if xpack:
+                            xp = self._pair(xs_rep[0][kk], xs_rep[1][kk], stmt)
+                            wv = f"{vecs[v]}.{comp[f % vw]}"
+                            stmt.append(f"{base}_{c}x = sf::fma2({xp}, make_float2({wv}, {wv}), "
+                                        f"{base}_{c}x);")
+                            continue
                         if c < 2 * npair:
                             if c % 2:
                                 continue
@@ -1172,6 +1279,9 @@ class _Gen:
                 for rep in range(self.R):
                     for c in range(2 * npair):
                         per_rep[rep][c] = f"{base}_p{c // 2}{self.sfx(rep)}.{'xy'[c % 2]}"
+                    if xpack:
+                        for c in range(n):
+                            per_rep[rep][c] = f"{base}_{c}x.{'xy'[rep]}"
             else:
                 for j in range(n):
                     for rep in range(self.R):
@@ -1210,7 +1320,7 @@ class _Gen:
         if id(o) in self.needed:
             # store right at the definition so the value's registers free up
             self._store(lines, o, per_rep)
-        self.body.append("    " + "\n    ".join(lines))
+        self.body.append(self._fill("    " + "\n    ".join(lines)))
 
 
 def _unflatten(f: int, shape) -> List[int]:
@@ -1263,7 +1373,10 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
            "__grid_constant__ Params a) {"]
     loads = [x for x in g.smem if "int q" in x]
     decls = [x for x in g.smem if "int q" not in x]
-    if g.pool_size:
+    if g.pool_size and g.cpool:
+        # keep the pool symbol in the module (it is referenced only from asm)
+        decls.append('  asm volatile("" :: "l"((const void*)cpool));')
+    elif g.pool_size:
         decls.append(f"  __shared__ __align__(16) unsigned char smem_pool[{g.pool_size}];\n"
                      "  const unsigned sp = sf::saddr(smem_pool);")
     src += decls + loads
@@ -1292,7 +1405,14 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
     if stores:
         src.append("    " + "\n    ".join(stores))
     src.append("  }\n}\n")
-    core = "\n".join(src)
+    head = ""
+    rp.cpool = None
+    if g.cpool and g.pool_size:
+        size = -(-g.pool_size // 16) * 16
+        head = ("#define SF_CPOOL 1\n"
+                f"__constant__ __align__(16) unsigned char cpool[{size}];\n")
+        rp.cpool = (size, list(g.cp_entries))
+    core = head + "\n".join(src)
     name = "sf_rows_" + hashlib.sha1(core.encode()).hexdigest()[:16]
-    source = '#include "sf_ops.cuh"\n' + core.replace("KNAME", name)
+    source = head + '#include "sf_ops.cuh"\n' + "\n".join(src).replace("KNAME", name)
     return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr

@@ -51,7 +51,7 @@ def test_headline_program_eager_equals_staged_bitwise_1e5():
             progs[mode] = _prog(s)
     for e, g in zip(outs["eager"], outs["staged"]):
         assert e.tobytes() == g.tobytes()
-    assert progs["staged"].n_launches == 2  # what bench.py times
+    assert progs["staged"].n_launches == 2  # uniform + row kernel: what bench.py times
     assert len(progs["staged"].segments) == 1
 
 

@@ -92,8 +92,8 @@ def test_l2hmc_staged_row_program():
     assert len(prog.segments) == 1
 
 
-@pytest.mark.parametrize("replicas", [1, 2])
-def test_rerolled_loop_bitwise_equals_eager(replicas, monkeypatch):
+@pytest.mark.parametrize("replicas,const_pool", [(1, False), (2, False), (1, True), (2, True)])
+def test_rerolled_loop_bitwise_equals_eager(replicas, const_pool, monkeypatch):
     """A traced Python loop with per-step weights and a shared bias: the staged
     row program re-rolls it (carried rows, stacked per-step weights, exported
     last step) and must match the eager per-op kernels bit for bit — with one
@@ -102,6 +102,7 @@ def test_rerolled_loop_bitwise_equals_eager(replicas, monkeypatch):
     from paper_1903_01855_b200 import rowfuse
 
     monkeypatch.setattr(rowfuse, "ROW_REPLICAS", replicas)
+    monkeypatch.setattr(rowfuse, "CONST_POOL", const_pool)
     plugins.install()
     rng = np.random.default_rng(3)
     B, D, steps = 1000, 6, 7
