@@ -30,6 +30,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+_OPENBLAS_ENV = os.environ.get("OPENBLAS_NUM_THREADS")
 FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived nominal FP32 SIMT peak
 
 
@@ -41,6 +42,13 @@ def _args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--chains", type=int, default=100000)
     ap.add_argument("--quick", action="store_true", help="skip the extra workloads")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="skip the same-seed eager==staged gate before timing")
+    # the reference's benchmark contract (stageflow/cli.py bench): with
+    # --workload, run paper_1903_01855_b200.benchmark instead of the headline
+    from paper_1903_01855_b200.benchmark import add_bench_args
+
+    add_bench_args(ap, required=False, warmup=False)
     return ap.parse_args()
 
 
@@ -50,6 +58,16 @@ def _peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def _compute_peaks():
+    """FP32 SIMT and tcgen05 peaks measured on a B200 by tools/peaks.cu
+    (profiles/r02_peaks.json); MEASURED_PEAKS.json has HBM and bf16 only."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_peaks.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 # ---------------------------------------------------------------------------
@@ -191,56 +209,116 @@ def graph_work(gf):
 # ---------------------------------------------------------------------------
 
 
-def _port_shard(args):
-    chains, seed, transitions = args
-    import numpy as np
+_PORT = None
 
+
+def _port_init(chains, seed):
+    global _PORT
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import workloads_np
 
-    m = workloads_np.L2HMC(chains, seed=seed, runtime_seed=seed)
+    _PORT = workloads_np.L2HMC(chains, seed=seed, runtime_seed=seed)
+
+
+def _port_step(_=None):
     t = time.perf_counter()
-    for _ in range(transitions):
-        m.transition()
+    _PORT.transition()
     return time.perf_counter() - t
 
 
-def cpu_port_rate(chains: int, transitions: int, workers: int):
-    """samples/s of the NumPy oracle port, chains sharded over `workers` processes."""
-    import multiprocessing as mp
+class PortPool:
+    """The NumPy oracle port of the L2HMC transition (oracle/workloads_np.py),
+    chains sharded contiguously over `workers` persistent processes (created
+    once, before any timed step; each holds its shard's state)."""
 
-    per = max(1, chains // workers)
-    jobs = [(per, 1000 + i, transitions) for i in range(workers)]
-    t = time.perf_counter()
-    if workers == 1:
-        _port_shard(jobs[0])
-    else:
-        with mp.get_context("fork").Pool(workers) as pool:
-            pool.map(_port_shard, jobs)
-    dt = time.perf_counter() - t
-    return per * workers * transitions / dt, dt
+    def __init__(self, chains: int, workers: int):
+        import multiprocessing as mp
+
+        self.chains, self.workers = chains, workers
+        per = -(-chains // workers)
+        sizes = [min(per, chains - i * per) for i in range(workers)]
+        sizes = [n for n in sizes if n > 0]
+        self.pools = []
+        if len(sizes) == 1:
+            _port_init(sizes[0], 1000)
+        else:
+            ctx = mp.get_context("fork")
+            self.pools = [ctx.Pool(1, initializer=_port_init, initargs=(n, 1000 + i))
+                          for i, n in enumerate(sizes)]
+            for p in self.pools:  # fork + build the shard before timing
+                p.apply(os.getpid)
+
+    def step(self) -> float:
+        """One transition of every chain; returns the wall time."""
+        t = time.perf_counter()
+        if not self.pools:
+            _port_step()
+        else:
+            for r in [p.apply_async(_port_step) for p in self.pools]:
+                r.get()
+        return time.perf_counter() - t
+
+    def close(self):
+        for p in self.pools:
+            p.terminate()
+
+
+def host_info() -> dict:
+    import numpy as np
+
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")),
+                         "")
+    except OSError:
+        pass
+    blas = ""
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg["Build Dependencies"]["blas"]
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:  # noqa: BLE001 - informational only
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__, "blas": blas,
+            "OPENBLAS_NUM_THREADS": _OPENBLAS_ENV or "unset; 1 per port process (bench.py)"}
+
+
+def cpu_port_rates(chains: int, steps: int, warmup: int = 1):
+    """All-cores and one-process samples/s of the port at `chains` chains."""
+    cores = os.cpu_count() or 1
+    pool = PortPool(chains, cores)
+    try:
+        for _ in range(warmup):
+            pool.step()
+        dts = [pool.step() for _ in range(steps)]
+    finally:
+        pool.close()
+    all_cores = chains * steps / sum(dts)
+    one = PortPool(chains, 1)
+    dt1 = one.step()
+    return {"all_cores": all_cores, "all_cores_s_per_step": sum(dts) / steps,
+            "workers_1": chains / dt1, "workers_1_s_per_step": dt1, "cores": cores}
 
 
 def run_reference(a, rank, world):
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
-    sample = min(a.chains, 20000)
-    rates = []
-    for i in range(a.warmup + a.steps):
-        r, _ = cpu_port_rate(sample, 1, cores)
-        if i >= a.warmup:
-            rates.append(r)
-    value = sum(rates) / len(rates)
+    r = cpu_port_rates(a.chains, a.steps, a.warmup)
+    value = r["all_cores"]
+    sample = (f"the full config: {a.chains} chains x {a.steps} transitions (1 transition per "
+              f"step), numpy oracle port (oracle/workloads_np.py L2HMC, pinned to the reference "
+              f"run at 1e5 chains) sharded over {r['cores']} persistent processes")
     line = {
         "impl": "reference", "metric": "l2hmc_samples_per_sec", "value": value,
         "unit": "samples/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": r["all_cores_s_per_step"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": "l2hmc_sampler_staged", "chains_per_gpu": a.chains,
-                   "leapfrog_steps": 10, "x_dim": 2, "hidden": 10},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} chains x 1 transition per step, numpy oracle port "
-                                   f"(oracle/workloads_np.py L2HMC) sharded over {cores} processes"},
+                   "leapfrog_steps": 10, "x_dim": 2, "hidden": 10, "same_config": True},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": r["cores"], "kind": "port",
+                         "sample": sample, "workers_1": r["workers_1"], "host": host_info()},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -252,6 +330,23 @@ def run_reference(a, rank, world):
 # ---------------------------------------------------------------------------
 
 
+def gate_headline(sf, plugins, l2hmc, chains, seed, rank, transitions=1):
+    """Eager and staged runs of the benchmarked program (same seeds, device
+    Philox) must agree bit for bit before anything is timed."""
+    import numpy as np
+
+    outs = {}
+    for mode in ("eager", "staged"):
+        sf.init_runtime(sf.RuntimeOptions(seed=seed))
+        plugins.install()
+        s = l2hmc.L2HMCSampler(sf, chains, mode, seed=rank)
+        outs[mode] = np.stack([s.run_iteration() for _ in range(transitions)])
+    diff = float(np.max(np.abs(outs["eager"].astype(np.float64) - outs["staged"])))
+    return {"passed": outs["eager"].tobytes() == outs["staged"].tobytes(),
+            "transitions": transitions, "chains": chains, "max_abs_diff": diff,
+            "criterion": "bitwise (reference gate: 1e-5)"}
+
+
 def run_ours(a, rank, world, dist):
     import numpy as np
     import torch
@@ -261,6 +356,16 @@ def run_ours(a, rank, world, dist):
     from paper_1903_01855_b200.workloads import l2hmc
 
     assert _native.device_count() > 0, "no CUDA device"
+    gate = None
+    if not a.no_gate:
+        # the reference refuses to time without a same-seed eager == staged
+        # check (stageflow/bench.py:216-234); here on the timed config itself
+        gate = gate_headline(sf, plugins, l2hmc, a.chains, 1234 + rank, rank)
+        if not gate["passed"]:
+            if rank == 0:
+                print(json.dumps({"metric": "l2hmc_samples_per_sec", "error": "gate failed",
+                                  "gate": gate}), flush=True)
+            sys.exit(2)
     sf.init_runtime(sf.RuntimeOptions(seed=1234 + rank))
     plugins.install()
     dev = 0
@@ -327,17 +432,23 @@ def run_ours(a, rank, world, dist):
     # full capture of this configuration (profiles/r01i_l2hmc_rows_full.md)
     traffic = None
     try:
-        tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                          "r01i_rows_traffic.json")
-        with open(tp) as fh:
-            traffic = json.load(fh)["dram_bytes_per_launch"]
+        for name in ("r02_rows_traffic.json", "r01i_rows_traffic.json"):
+            tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+            if os.path.exists(tp):
+                with open(tp) as fh:
+                    traffic = json.load(fh)["dram_bytes_per_launch"]
+                break
     except (OSError, ValueError, KeyError):
         pass
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": FFMA_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FFMA_PEAK_TFLOPS, "traffic": traffic,
+    cpk = _compute_peaks()
+    ffma_peak = cpk.get("ffma_tflops", FFMA_PEAK_TFLOPS)
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": ffma_peak,
+                "unit": "TFLOP/s", "frac": achieved / ffma_peak, "traffic": traffic,
                 "traffic_unit": "DRAM bytes per row-kernel launch (ncu)",
-                "peak_kind": "derived nominal FP32 SIMT (148 SM x 128 lanes x 2 x 1.965 GHz); "
-                             "the row program has no tensor-core-shaped work (K<=10 per chain)",
+                "peak_kind": ("measured FP32 SIMT FFMA peak (tools/peaks.cu, profiles/r02_peaks.json;"
+                              " FFMA2 measured the same 74 TF)" if "ffma_tflops" in cpk else
+                              "derived nominal FP32 SIMT (148 SM x 128 lanes x 2 x 1.965 GHz)")
+                             + "; the row program has no tensor-core-shaped work (K<=10 per chain)",
                 "kernels_per_step": len(jit_ms), "kernel_ms_per_step": kern_ms,
                 "algorithmic_flops_per_step": flops_per_step,
                 "flops_per_chain": flops_per_step / B,
@@ -389,12 +500,12 @@ def run_ours(a, rank, world, dist):
             extra["c5_resnet50_dp"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     cpu = None
     if rank == 0 and world == 1:
-        cores = os.cpu_count() or 1
-        sample = 20000
-        r, dt = cpu_port_rate(sample, 1, cores)
-        cpu = {"value": r, "unit": "samples/s", "cores": cores, "kind": "port",
-               "sample": f"{sample} chains x 1 transition ({dt:.1f}s), numpy oracle port sharded "
-                         f"over {cores} processes"}
+        r = cpu_port_rates(B, 3, 1)
+        cpu = {"value": r["all_cores"], "unit": "samples/s", "cores": r["cores"], "kind": "port",
+               "sample": f"the full config: {B} chains x 3 transitions "
+                         f"({r['all_cores_s_per_step']:.2f} s each), numpy oracle port sharded "
+                         f"over {r['cores']} persistent processes",
+               "workers_1": r["workers_1"], "host": host_info()}
     if rank != 0:
         return
     line = {
@@ -407,7 +518,7 @@ def run_ours(a, rank, world, dist):
                    "parallelism": f"dp{world} (independent chains, no collective)",
                    "l2_flush": "256 MiB fill between timed steps",
                    "rng": "device Philox"},
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gate": gate,
         "gpu_launches": launches, "gpu_launches_per_step": launches / a.steps,
         "clocks": clk.summary(), "trace_and_compile_s": warm_s,
         "graph_ops": n_graph_ops, "native_launches_per_step": prog.n_launches,
@@ -628,6 +739,12 @@ def main():
     if a.impl == "reference":
         run_reference(a, rank, world)
         return
+    if a.workload:
+        # the reference's benchmark contract (stageflow bench --workload ...)
+        from paper_1903_01855_b200.benchmark import run_cli
+
+        a.bench_warmup = a.warmup
+        sys.exit(run_cli(a))
     if world > 1:
         os.environ["CUDA_VISIBLE_DEVICES"] = str(local)
     import torch

@@ -509,6 +509,17 @@ def copy_p2p(dst_dev: int, dst: int, src_dev: int, src: int, nbytes: int) -> Non
         raise _err(_lib, rc, "sf_memcpy_p2p")
 
 
+
+def device_name(dev: int) -> str:
+    """Short device description for reports, e.g. "sm_100 148SM 178GB"."""
+    L = require_device()
+    sms, ma, mi, mem = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0), ctypes.c_size_t(0)
+    rc = L.sf_device_info(dev, ctypes.byref(sms), ctypes.byref(ma), ctypes.byref(mi),
+                          ctypes.byref(mem))
+    if rc:
+        raise _err(L, rc, "sf_device_info")
+    return f"sm_{ma.value}{mi.value} {sms.value}SM {mem.value >> 30}GB"
+
 def sync(dev: int) -> None:
     L = require_device()
     rc = L.sf_device_sync(dev)

@@ -15,6 +15,8 @@ ops registered with its ``register_op``, oracle/ref_plugins.py):
   headline batch, 100,000 chains, for three transitions: the first 4096
   chains of the state and accept probabilities, and float64 sums over all
   chains;
+* ``microop_*``: the reference's microop_loop workload — values, the staged
+  graph's SGF1 bytes, and run_benchmark's trace/cache/copy counters;
 * ``resnet_c4_{f32,f64}_*``: ResNet-50 at config C4 (batch 32, 224x224x3,
   seed 0) — the loss and the gradients of all 161 parameters of one tape
   step, in float32 and float64: per-parameter float64 norms and sums, and the
@@ -110,8 +112,28 @@ def resnet_c4(out):
     out["resnet_c4_params"] = np.array(RESNET_PARAMS)
 
 
+def microop_fixtures(out):
+    """_MicroOpLoop (stageflow/bench.py:186-206): values, graph bytes, and the
+    reference harness's trace/copy counters (run_benchmark, :237-273)."""
+    from stageflow import bench as ref_bench
+
+    for mode in ("eager", "staged"):
+        _fresh()
+        cfg = ref_bench.BenchConfig(workload="microop_loop", mode=mode, batch_size=1,
+                                    iterations=3, warmup=1, repeats=2)
+        wl = ref_bench._MicroOpLoop(cfg, mode)
+        out[f"microop_{mode}_values"] = np.array([wl.run_iteration() for _ in range(3)])
+        if mode == "staged":
+            gf = wl.staged_functions[0].cached_functions()[0].graph
+            out["microop_graph"] = np.frombuffer(serialize(gf), dtype=np.uint8)
+        _fresh()
+        rep = ref_bench.run_benchmark(cfg)
+        out[f"microop_{mode}_report"] = np.array([rep.trace_count, rep.cache_size, rep.copies])
+
+
 def main():
     out = {}
+    microop_fixtures(out)
     l2hmc_graphs(out)
     l2hmc_headline(out)
     if "--skip-resnet" not in sys.argv:
