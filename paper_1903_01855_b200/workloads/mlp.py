@@ -21,6 +21,7 @@ def _f32(arr) -> sf.Tensor:
 class MLPTrain:
     IN, HIDDEN, OUT = 128, 256, 1
     LR = 1e-3
+    gate_tol = 1e-5
 
     def __init__(self, batch: int, mode: str, seed: int = 0):
         rng = np.random.default_rng(seed)
@@ -60,3 +61,6 @@ class MLPTrain:
 
     def run_iteration(self) -> float:
         return float(self.step())
+
+    def cache_size(self) -> int:
+        return sum(pf.cache_size for pf in self.staged_functions)
