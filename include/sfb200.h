@@ -114,6 +114,43 @@ typedef struct sf_ew_desc {
 } sf_ew_desc;
 
 int sf_elementwise(int dev, const sf_ew_desc* desc, void** out);
+
+/* ------------------------------------------------------- eager launch queue
+ * Small primitives are queued as compact descriptors and executed in push
+ * order by ONE launch of an interpreter kernel (a single CTA, one barrier
+ * between consecutive ops, the same per-element functions and matmul
+ * contract as the one-op kernels: queued and direct results are
+ * bit-identical).  The queue is flushed when full, by sf_queue_flush, and
+ * before any other call that enqueues work on the device's stream (copies,
+ * syncs, plan runs, graph launches and captures), so stream order is push
+ * order.  Ops too large for the queue (> max_numel elements, rank > 4 after
+ * collapsing, k > 256 matmuls) flush it and launch directly.
+ * sf_elementwise, sf_matmul, sf_transpose2d and sf_fill go through it.
+ * Replaces: the per-op np.* call of _dispatch_eager -> kernel,
+ * stageflow/ops.py:318-347 (kernels.py:116-219); the reference has no queue
+ * (every op runs to completion inside dispatch). */
+#define SF_QOP_EW 0
+#define SF_QOP_MATMUL 1
+typedef struct sf_op_desc {
+  int32_t kind;   /* SF_QOP_* */
+  int32_t op;     /* EW: SF_OP_*; MATMUL: bit0 = A transposed, bit1 = B transposed */
+  int32_t dtype;  /* input dtype */
+  int32_t ndim;   /* EW: output rank */
+  int32_t n_in;   /* EW: 1..3 */
+  int32_t pad;
+  int64_t m, n, k;  /* MATMUL: C[m,n] = op(A)[m,k] @ op(B)[k,n] */
+  const void* in[3];  /* NULL => immediate imm[i] (EW) */
+  double imm[3];
+  int64_t shape[SF_MAX_DIMS];
+  int64_t strides[3][SF_MAX_DIMS];
+} sf_op_desc;
+/* Queue (or, when it does not fit, launch) one primitive; allocates *out
+ * from the caching allocator when NULL. */
+int sf_queue_push(int dev, const sf_op_desc* desc, void** out);
+int sf_queue_flush(int dev);
+/* max_ops (<= 64) per launch, 0 disables queueing; max_numel per op. */
+int sf_queue_config(int dev, int max_ops, int64_t max_numel);
+int sf_queue_stats(int dev, uint64_t* pushed, uint64_t* flushes);
 /* op: 0 = sum, 1 = mean.  axes_mask bit i set => axis i reduced. */
 int sf_reduce(int dev, int op, int dtype, int ndim, const int64_t* shape, uint32_t axes_mask,
               const void* in, void** out);

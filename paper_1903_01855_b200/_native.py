@@ -117,6 +117,11 @@ def _declare(lib: ctypes.CDLL) -> None:
                                                ctypes.POINTER(ctypes.c_double),
                                                ctypes.POINTER(ctypes.c_uint64)]),
         "sf_launch_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
+        "sf_queue_push": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _PVP]),
+        "sf_queue_flush": (ctypes.c_int, [ctypes.c_int]),
+        "sf_queue_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64]),
+        "sf_queue_stats": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
+                                           ctypes.POINTER(ctypes.c_uint64)]),
         "sf_while_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
         "sf_cond_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
         "sf_graph_create": (ctypes.c_int, [ctypes.c_int, _PVP]),
@@ -149,7 +154,7 @@ EXPORTED_SYMBOLS = (
     "sf_split_tf32", "sf_im2col_split", "sf_while_create", "sf_cond_create", "sf_graph_create",
     "sf_while_buffer",
     "sf_while_capture_begin", "sf_while_set_cond", "sf_while_capture_end", "sf_while_launch",
-    "sf_while_destroy",
+    "sf_while_destroy", "sf_queue_push", "sf_queue_flush", "sf_queue_config", "sf_queue_stats",
 )
 
 
@@ -571,6 +576,29 @@ def launch_count(dev: int) -> int:
     c = ctypes.c_uint64(0)
     L.sf_launch_count(dev, ctypes.byref(c))
     return c.value
+
+
+def queue_flush(dev: int) -> None:
+    """Launch what the eager launch queue holds (csrc/sf_queue.cu)."""
+    rc = lib().sf_queue_flush(dev)
+    if rc:
+        raise _err(_lib, rc, "sf_queue_flush")
+
+
+def queue_config(dev: int, max_ops: int, max_numel: int = 16384) -> None:
+    """Ops per queue launch (0 disables queueing) and the largest queued op."""
+    rc = lib().sf_queue_config(dev, max_ops, max_numel)
+    if rc:
+        raise _err(_lib, rc, "sf_queue_config")
+
+
+def queue_stats(dev: int):
+    """(ops pushed into the queue, queue launches) since sf_init."""
+    a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    rc = lib().sf_queue_stats(dev, ctypes.byref(a), ctypes.byref(b))
+    if rc:
+        raise _err(_lib, rc, "sf_queue_stats")
+    return a.value, b.value
 
 
 def rng_seed(dev: int, seed: int) -> None:

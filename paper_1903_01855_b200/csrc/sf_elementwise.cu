@@ -428,28 +428,26 @@ static int out_dtype_for(int op, int dtype) {
 }
 
 extern "C" int sf_elementwise(int dev, const sf_ew_desc* desc, void** out) {
-  Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  // small primitives go through the launch queue (sf_queue.cu); the rest
+  // launch directly after the queue is flushed
   if (desc->ndim < 0 || desc->ndim > SF_MAX_DIMS || desc->n_in < 1 || desc->n_in > 3) {
     set_error("sf_elementwise: bad descriptor");
     return SF_ERR_INVALID;
   }
-  long long n = 1;
-  for (int i = 0; i < desc->ndim; ++i) n *= desc->shape[i];
-  const int odt = desc->op == SF_OP_SELECT ? desc->dtype : out_dtype_for(desc->op, desc->dtype);
-  bool fresh = false;
-  if (*out == nullptr) {
-    SF_TRY(d->alloc.alloc(dev, (size_t)n * dtype_size(odt), out));
-    fresh = true;
+  sf_op_desc q;
+  std::memset(&q, 0, sizeof(q));
+  q.kind = SF_QOP_EW;
+  q.op = desc->op;
+  q.dtype = desc->dtype;
+  q.ndim = desc->ndim;
+  q.n_in = desc->n_in;
+  for (int j = 0; j < 3; ++j) {
+    q.in[j] = desc->in[j];
+    q.imm[j] = desc->imm[j];
   }
-  const int64_t* strides[3] = {desc->strides[0], desc->strides[1], desc->strides[2]};
-  int st = launch_elementwise(d, desc->op, desc->dtype, desc->ndim, desc->shape, *out, desc->in,
-                              strides, desc->imm, desc->n_in);
-  if (st != SF_OK && fresh) {
-    d->alloc.release(*out);
-    *out = nullptr;
-  }
-  return st;
+  std::memcpy(q.shape, desc->shape, sizeof(q.shape));
+  std::memcpy(q.strides, desc->strides, sizeof(q.strides));
+  return sf_queue_push(dev, &q, out);
 }
 
 extern "C" int sf_cast(int dev, int src_dtype, int dst_dtype, int64_t n, const void* in, void** out) {

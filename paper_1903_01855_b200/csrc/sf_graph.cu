@@ -111,6 +111,7 @@ int sf_while_capture_begin(void* wp, int part) {
     set_error("sf_while_capture_begin: capture already open or graph already built");
     return SF_ERR_INVALID;
   }
+  SF_TRY(queue_flush(w->d));  // queued eager ops precede the capture
   w->d->alloc.begin_capture();
   cudaError_t e = cudaStreamBeginCaptureToGraph(w->d->stream,
                                                 part ? w->body[part - 1] : w->graph, nullptr,
@@ -192,6 +193,7 @@ int sf_while_launch(void* wp) {
       return SF_ERR_CUDA;
     }
   }
+  SF_TRY(queue_flush(w->d));
   SF_CHECK_CUDA(cudaGraphLaunch(w->exec, w->d->stream));
   count_launch(w->d->id);
   return SF_OK;
@@ -201,6 +203,7 @@ int sf_while_destroy(void* wp) {
   auto* w = (WhileGraph*)wp;
   if (!w) return SF_OK;
   // the graph may still be executing: wait before its blocks are reused
+  queue_flush(w->d);
   cudaStreamSynchronize(w->d->stream);
   if (w->exec) cudaGraphExecDestroy(w->exec);
   if (w->graph) cudaGraphDestroy(w->graph);

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -84,6 +85,7 @@ class Allocator {
   void begin_capture();
   void end_capture(std::vector<std::pair<void*, size_t>>* owned);
   void give_back(const std::vector<std::pair<void*, size_t>>& owned);
+  bool capturing() const { return capturing_; }
 
  private:
   static size_t round_size(size_t bytes);
@@ -94,6 +96,16 @@ class Allocator {
   bool capturing_ = false;
   std::vector<std::pair<void*, size_t>> cap_log_;
   std::unordered_map<size_t, std::vector<void*>> cap_free_;
+};
+
+// Eager launch queue (sf_queue.cu): compact descriptors of small primitives,
+// executed in push order by one interpreter-kernel launch per flush.
+constexpr int kQueueDims = 4;
+constexpr int kQueueMaxOps = 64;
+constexpr int kQueueThreads = 512;
+struct QOp;  // sf_queue.cu
+struct QOpSlot {
+  alignas(8) unsigned char bytes[152];
 };
 
 struct Device {
@@ -128,10 +140,24 @@ struct Device {
   unsigned long long rng_seed = 0;
   unsigned long long rng_offset = 0;
   std::mutex rng_mu;
+  // eager launch queue: q_pending != 0 while q_ops is non-empty (checked
+  // without the lock by every entry point that enqueues stream work)
+  std::mutex q_mu;
+  std::vector<QOpSlot> q_ops;
+  std::atomic<int> q_pending{0};
+  int q_max_ops = kQueueMaxOps;
+  long long q_max_numel = 16384;
+  unsigned long long q_pushed = 0, q_flushes = 0;
 };
 
 Device* device(int dev);  // nullptr if invalid
-int ensure_device(int dev, Device** out);  // sets current device, validates
+// sets the current device and validates; flushes the device's launch queue
+// (every entry point that enqueues stream work calls this first)
+int ensure_device(int dev, Device** out);
+// the same without the flush (allocation, counters, queue pushes)
+int ensure_device_noflush(int dev, Device** out);
+int queue_flush(Device* d);
+int queue_flush_dev(int dev);
 size_t dtype_size(int dtype);
 void count_launch(int dev, unsigned long long n = 1);
 

@@ -205,8 +205,21 @@ using namespace sfrt;
 
 extern "C" int sf_matmul(int dev, int dtype, int64_t m, int64_t n, int64_t k, const void* a,
                          int trans_a, const void* b, int trans_b, void** out) {
-  Device* d;
-  SF_TRY(ensure_device(dev, &d));
-  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(m * n) * dtype_size(dtype), out));
-  return launch_matmul(d, dtype, m, n, k, a, trans_a, b, trans_b, *out);
+  if (dtype != SF_DTYPE_F32 && dtype != SF_DTYPE_F64) {
+    set_error("matmul requires float tensors");
+    return SF_ERR_INVALID;
+  }
+  // tiny products go through the launch queue (same sequential-k FMA order)
+  sf_op_desc q;
+  std::memset(&q, 0, sizeof(q));
+  q.kind = SF_QOP_MATMUL;
+  q.op = (trans_a ? 1 : 0) | (trans_b ? 2 : 0);
+  q.dtype = dtype;
+  q.n_in = 2;
+  q.m = m;
+  q.n = n;
+  q.k = k;
+  q.in[0] = a;
+  q.in[1] = b;
+  return sf_queue_push(dev, &q, out);
 }

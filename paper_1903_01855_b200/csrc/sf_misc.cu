@@ -213,14 +213,45 @@ extern "C" {
 
 int sf_transpose2d(int dev, int dtype, int64_t rows, int64_t cols, const void* in, void** out) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
+  if (rows * cols <= d->q_max_numel) {
+    // small: a strided identity copy through the launch queue
+    sf_op_desc q;
+    std::memset(&q, 0, sizeof(q));
+    q.kind = SF_QOP_EW;
+    q.op = SF_OP_IDENTITY;
+    q.dtype = dtype;
+    q.ndim = 2;
+    q.n_in = 1;
+    q.in[0] = in;
+    q.shape[0] = cols;
+    q.shape[1] = rows;
+    q.strides[0][0] = 1;
+    q.strides[0][1] = cols;
+    return sf_queue_push(dev, &q, out);
+  }
+  SF_TRY(queue_flush(d));
   if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(rows * cols) * dtype_size(dtype), out));
   return launch_transpose2d(d, dtype, rows, cols, in, *out);
 }
 
 int sf_fill(int dev, int dtype, int64_t n, double value, void** out) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
+  if (n <= d->q_max_numel) {
+    // small: an identity of an immediate through the launch queue
+    sf_op_desc q;
+    std::memset(&q, 0, sizeof(q));
+    q.kind = SF_QOP_EW;
+    q.op = SF_OP_IDENTITY;
+    q.dtype = dtype;
+    q.ndim = 1;
+    q.n_in = 1;
+    q.imm[0] = value;
+    q.shape[0] = n;
+    return sf_queue_push(dev, &q, out);
+  }
+  SF_TRY(queue_flush(d));
   if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)n * dtype_size(dtype), out));
   return launch_fill(d, dtype, n, value, *out);
 }

@@ -45,6 +45,13 @@ Device* device(int dev) {
 static thread_local int t_current = -1;
 
 int ensure_device(int dev, Device** out) {
+  SF_TRY(ensure_device_noflush(dev, out));
+  Device* d = *out;
+  if (d->q_pending.load(std::memory_order_acquire)) return queue_flush(d);
+  return SF_OK;
+}
+
+int ensure_device_noflush(int dev, Device** out) {
   if (!g_inited) {
     int n = 0;
     SF_TRY(sf_init(&n));
@@ -122,7 +129,9 @@ int Allocator::alloc(int dev, size_t bytes, void** p) {
       set_error("device " + std::to_string(dev) + ": out of memory during graph capture");
       return SF_ERR_OOM;
     }
-    // Return the cache to the driver and retry once.
+    // Return the cache to the driver and retry once (queued ops may still
+    // read cached blocks: launch them first).
+    queue_flush_dev(dev);
     cudaDeviceSynchronize();
     trim();
     e = cudaMalloc(&q, sz);
@@ -257,7 +266,7 @@ int sf_init(int* n_devices) {
 
 int sf_device_info(int dev, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
   cudaDeviceProp prop;
   SF_CHECK_CUDA(cudaGetDeviceProperties(&prop, dev));
   if (sm_count) *sm_count = prop.multiProcessorCount;
@@ -301,7 +310,7 @@ int sf_device_sync(int dev) {
 
 int sf_alloc(int dev, size_t bytes, void** p) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
   return d->alloc.alloc(dev, bytes, p);
 }
 
@@ -316,14 +325,14 @@ int sf_free(int dev, void* p) {
 
 int sf_reduce_counters(int dev, void** counters) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
   *counters = d->red_counters;
   return SF_OK;
 }
 
 int sf_mem_stats(int dev, size_t* in_use, size_t* cached) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
   if (in_use) *in_use = d->alloc.bytes_in_use();
   if (cached) *cached = d->alloc.bytes_cached();
   return SF_OK;
@@ -499,7 +508,7 @@ int sf_memcpy_p2p(int dst_dev, void* dst, int src_dev, const void* src, size_t b
 
 int sf_rng_seed(int dev, uint64_t seed) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
   std::lock_guard<std::mutex> lk(d->rng_mu);
   d->rng_seed = seed;
   d->rng_offset = 0;
@@ -508,7 +517,7 @@ int sf_rng_seed(int dev, uint64_t seed) {
 
 int sf_rng_reserve(int dev, uint64_t n, uint64_t* offset) {
   Device* d;
-  SF_TRY(ensure_device(dev, &d));
+  SF_TRY(ensure_device_noflush(dev, &d));
   std::lock_guard<std::mutex> lk(d->rng_mu);
   *offset = d->rng_offset;
   d->rng_offset += n;

@@ -678,7 +678,7 @@ class _GraphBuffer(_native.DeviceBuffer):
         self.token = token
 
     def __del__(self):
-        pass
+        self.ptr = 0  # the graph owns the memory: nothing to release
 
 
 class _Token:

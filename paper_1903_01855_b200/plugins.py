@@ -14,7 +14,7 @@ from __future__ import annotations
 
 from typing import List
 
-from . import _native, dtypes
+from . import _fastpath, _native, dtypes
 from .dtypes import DType
 from .errors import KernelError
 from .kernels import _bcast, launch_ew, ordinal_of
@@ -35,6 +35,7 @@ def _float_unary(name):
             raise KernelError(f"{name} requires a float tensor, got {dt.value}")
         return [(dt, shape)]
 
+    _fastpath.mark_fast(kernel, _fastpath.K_EW1, _native.OP[name], _fastpath.F_FLOATS_ONLY)
     return kernel, infer
 
 
@@ -56,6 +57,8 @@ def _same_binary(name, out_bool=False):
             raise KernelError(f"{name} is not defined for boolean tensors")
         return [(DType.boolean if out_bool else da, _bcast(sa, sb))]
 
+    _fastpath.mark_fast(kernel, _fastpath.K_EW2, _native.OP[name],
+                        _fastpath.F_OUT_BOOL if out_bool else 0)
     return kernel, infer
 
 
@@ -239,7 +242,7 @@ def _w1(op):
         return dispatch(op, [_as_operand(x)])[0]
 
     fn.__name__ = op
-    return fn
+    return _fastpath.wrap(op, 1, fn)
 
 
 def _w2(op):
@@ -251,7 +254,7 @@ def _w2(op):
         return dispatch(op, [a, b])[0]
 
     fn.__name__ = op
-    return fn
+    return _fastpath.wrap(op, 2, fn)
 
 
 tanh = _w1("tanh")
