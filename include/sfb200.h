@@ -125,12 +125,16 @@ int sf_elementwise(int dev, const sf_ew_desc* desc, void** out);
  * syncs, plan runs, graph launches and captures), so stream order is push
  * order.  Ops too large for the queue (> max_numel elements, rank > 4 after
  * collapsing, k > 256 matmuls) flush it and launch directly.
- * sf_elementwise, sf_matmul, sf_transpose2d and sf_fill go through it.
+ * sf_elementwise, sf_matmul, sf_transpose2d, sf_fill and the short float
+ * reductions of sf_reduce (<= 1024 elements per output: one CRO chunk,
+ * evaluated by one warp per output with the same fold and butterfly) go
+ * through it.
  * Replaces: the per-op np.* call of _dispatch_eager -> kernel,
  * stageflow/ops.py:318-347 (kernels.py:116-219); the reference has no queue
  * (every op runs to completion inside dispatch). */
 #define SF_QOP_EW 0
 #define SF_QOP_MATMUL 1
+#define SF_QOP_REDUCE 2 /* op: 0 sum, 1 mean; m = axes mask (float dtypes) */
 typedef struct sf_op_desc {
   int32_t kind;   /* SF_QOP_* */
   int32_t op;     /* EW: SF_OP_*; MATMUL: bit0 = A transposed, bit1 = B transposed */

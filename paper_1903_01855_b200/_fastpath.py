@@ -178,7 +178,18 @@ def bootstrap() -> None:
         from . import ops, runtime
 
         ext.bootstrap(vars(runtime), runtime._local, configure, ops._dispatch_py,
-                      ops._operator_slow)
+                      ops._operator_slow, host_scalar)
+
+
+def host_scalar(value, dtype):
+    """The read-only 0-d host array the reference's ``_as_operand(value,
+    like)`` builds for a Python scalar (ops.py:370-383 -> tensor.py:138-162)."""
+    import numpy as np
+
+    from .tensor import _checked_host_array
+
+    arr = np.asarray(value, dtype=dtype.np_dtype)
+    return _checked_host_array(arr.reshape(-1), arr.shape, dtype)
 
 
 def wrap(name: str, arity: int, slow):

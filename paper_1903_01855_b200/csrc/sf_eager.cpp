@@ -746,8 +746,9 @@ PyObject* py_dispatch(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
   PyObject* name = args[0];
   PyObject* inputs = args[1];
   PyObject* attrs = nargs == 3 ? args[2] : Py_None;
-  PyObject* ctx = nullptr;
-  FastOp* f = PyUnicode_CheckExact(name) ? lookup(name) : nullptr;
+  // (fast_context binds the table to the live runtime first)
+  PyObject* ctx = fast_context();
+  FastOp* f = ctx && PyUnicode_CheckExact(name) ? lookup(name) : nullptr;
   if (f && (PyList_CheckExact(inputs) || PyTuple_CheckExact(inputs))) {
     PyObject* attr_arg = nullptr;
     bool attrs_ok = true;
@@ -760,7 +761,7 @@ PyObject* py_dispatch(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     bool tensors = n <= 3;
     for (Py_ssize_t i = 0; tensors && i < n; ++i)
       tensors = is_tensor(in[i]) && concrete(in[i]);
-    if (attrs_ok && tensors && (ctx = fast_context()) != nullptr) {
+    if (attrs_ok && tensors) {
       PyObject* canon = nullptr;
       PyObject* holder[3];  // keep the inputs alive across Python callbacks
       for (Py_ssize_t i = 0; i < n; ++i) holder[i] = Py_NewRef(in[i]);
@@ -823,10 +824,49 @@ bool scalar_imm(PyObject* x, int tag, double* out) {
   return false;
 }
 
+PyObject* g_host_scalar = nullptr;  // _fastpath.host_scalar(value, dtype) -> read-only 0-d array
+PyObject* g_scalar_cache = nullptr;  // (tag, value) -> that array
+PyObject* g_empty_shape = nullptr;
+
+// A fresh 0-d constant tensor holding `scalar` in `tag`'s dtype (reference
+// _as_operand -> tensor_from_host, ops.py:370-383); the immutable host
+// array is shared between tensors of the same value.
+PyObject* const_tensor(PyObject* scalar, int tag) {
+  PyObject* key = Py_BuildValue("(iO)", tag, scalar);
+  if (!key) return nullptr;
+  PyObject* arr = PyDict_GetItemWithError(g_scalar_cache, key);  // borrowed
+  if (arr) {
+    Py_INCREF(arr);
+  } else {
+    if (PyErr_Occurred()) {
+      Py_DECREF(key);
+      return nullptr;
+    }
+    arr = PyObject_CallFunctionObjArgs(g_host_scalar, scalar, g_dtypes[tag], nullptr);
+    if (!arr) {
+      Py_DECREF(key);
+      return nullptr;
+    }
+    if (PyDict_GET_SIZE(g_scalar_cache) > 4096) PyDict_Clear(g_scalar_cache);
+    if (PyDict_SetItem(g_scalar_cache, key, arr) < 0) {
+      Py_DECREF(key);
+      Py_DECREF(arr);
+      return nullptr;
+    }
+  }
+  Py_DECREF(key);
+  PyObject* t = new_tensor(g_dtypes[tag], g_empty_shape, nullptr, arr);
+  Py_DECREF(arr);
+  return t;
+}
+
 // A binary operation with the reference's operand coercion (_binary /
 // operator overloads, ops.py:370-485): Tensor (op) Tensor, or a Tensor with
 // a Python scalar taken "like" the tensor.  Returns NOT_FAST to defer.
-PyObject* fast_binary(FastOp* f, PyObject* a, PyObject* b) {
+PyObject* fast_binary(PyObject* name, PyObject* a, PyObject* b) {
+  PyObject* ctx = fast_context();
+  if (!ctx) return NOT_FAST;
+  FastOp* f = lookup(name);
   if (!f) return NOT_FAST;
   const bool at = is_tensor(a), bt = is_tensor(b);
   if ((at && !concrete(a)) || (bt && !concrete(b))) return NOT_FAST;
@@ -845,11 +885,20 @@ PyObject* fast_binary(FastOp* f, PyObject* a, PyObject* b) {
       psa = &sa;
     }
   }
-  PyObject* ctx = fast_context();
-  if (!ctx) return NOT_FAST;
-  // a scalar operand becomes a constant tensor the tape would record: defer
-  if ((psa || psb) && tapes_active(ctx)) return NOT_FAST;
-  PyObject* in[2] = {Py_NewRef(a), Py_NewRef(b)};
+  PyObject* in[2];
+  if ((psa || psb) && tapes_active(ctx)) {
+    // a watching tape records the scalar as a constant tensor input (the
+    // reference's _as_operand): build it (host bytes, no upload)
+    const int tag = tag_of(((TensorObj*)(at ? a : b))->dtype);
+    PyObject* c = const_tensor(at ? b : a, tag);
+    if (!c) return nullptr;
+    in[0] = at ? Py_NewRef(a) : c;
+    in[1] = at ? c : Py_NewRef(b);
+    psa = psb = nullptr;
+  } else {
+    in[0] = Py_NewRef(a);
+    in[1] = Py_NewRef(b);
+  }
   PyObject* out = run_fast(*f, in, 2, nullptr, psa, psb, nullptr);
   if (out && out != NOT_FAST && !finish(*f, ctx, in, 2, out, nullptr)) {
     Py_DECREF(out);
@@ -878,14 +927,14 @@ PyObject* FastWrapper_call(PyObject* o, PyObject* const* args, size_t nargsf, Py
   FastWrapper* w = (FastWrapper*)o;
   const Py_ssize_t n = PyVectorcall_NARGS(nargsf);
   if (!kw && n == w->arity && !PyErr_Occurred()) {
-    FastOp* f = lookup(w->name);
     PyObject* out = NOT_FAST;
-    if (f) {
-      if (n == 2) {
-        out = fast_binary(f, args[0], args[1]);
-      } else if (n == 1 && is_tensor(args[0]) && concrete(args[0])) {
-        PyObject* ctx = fast_context();
-        if (ctx) {
+    if (n == 2) {
+      out = fast_binary(w->name, args[0], args[1]);
+    } else if (n == 1 && is_tensor(args[0]) && concrete(args[0])) {
+      PyObject* ctx = fast_context();
+      FastOp* f = ctx ? lookup(w->name) : nullptr;
+      if (f) {
+        {
           PyObject* in[1] = {Py_NewRef(args[0])};
           out = run_fast(*f, in, 1, nullptr, nullptr, nullptr, nullptr);
           if (out && out != NOT_FAST && !finish(*f, ctx, in, 1, out, nullptr)) {
@@ -961,7 +1010,7 @@ PyObject* tensor_binop(int which, PyObject* a, PyObject* b, bool has_reflected) 
   const bool at = is_tensor(a);
   if (!at && !has_reflected) Py_RETURN_NOTIMPLEMENTED;
   PyObject* name = g_op_names[which];
-  PyObject* out = fast_binary(lookup(name), a, b);
+  PyObject* out = fast_binary(name, a, b);
   if (out != NOT_FAST) return out;
   if (PyErr_Occurred()) return nullptr;
   if (!g_binop_slow) Py_RETURN_NOTIMPLEMENTED;
@@ -1007,14 +1056,18 @@ PyNumberMethods Tensor_number = {};
 // ---------------------------------------------------------- configuration
 
 // bootstrap(rt_module_dict, thread_local, configure_cb, slow_dispatch,
-//           binop_slow): where to find the
+//           binop_slow, host_scalar): where to find the
 // live runtime (`_runtime` in paper_1903_01855_b200.runtime), the
 // per-thread context, and the Python function that (re)binds the fast path
 // when the live runtime changes (init_runtime).
 PyObject* py_bootstrap(PyObject*, PyObject* args) {
-  PyObject *rt_dict, *local, *cfg, *slow, *binop_slow;
-  if (!PyArg_ParseTuple(args, "O!OOOO", &PyDict_Type, &rt_dict, &local, &cfg, &slow, &binop_slow))
+  PyObject *rt_dict, *local, *cfg, *slow, *binop_slow, *host_scalar;
+  if (!PyArg_ParseTuple(args, "O!OOOOO", &PyDict_Type, &rt_dict, &local, &cfg, &slow,
+                        &binop_slow, &host_scalar))
     return nullptr;
+  Py_XSETREF(g_host_scalar, Py_NewRef(host_scalar));
+  if (!g_scalar_cache && !(g_scalar_cache = PyDict_New())) return nullptr;
+  if (!g_empty_shape && !(g_empty_shape = PyTuple_New(0))) return nullptr;
   Py_XSETREF(g_rt_dict, Py_NewRef(rt_dict));
   Py_XSETREF(g_local, Py_NewRef(local));
   Py_XSETREF(g_configure, Py_NewRef(cfg));

@@ -180,6 +180,16 @@ int launch_dropout(Device* d, int dtype, int64_t n, const void* x, const void* u
                    int u_dtype, double rate, void* out, void* mask);
 int launch_cast(Device* d, int src_dtype, int dst_dtype, int64_t n, const void* in, void* out);
 
+// reduce_sum/mean geometry: kept and reduced dims (size-1 dims dropped,
+// contiguous dims merged), element strides of a row-major input
+struct RedGeom {
+  long long n_out, r;
+  int kept_nd, red_nd;
+  long long kept_shape[SF_MAX_DIMS], kept_stride[SF_MAX_DIMS];
+  long long red_shape[SF_MAX_DIMS], red_stride[SF_MAX_DIMS];
+};
+void reduce_geometry(int ndim, const int64_t* shape, uint32_t axes_mask, RedGeom* g);
+
 // Row-kernel constant pool (sf_plan.cpp step kind 1 with a pool section):
 // gather the kernel's uniform operands into `image` at their pool offsets
 // (rows of N elements padded to Np), then the image is copied into the

@@ -111,6 +111,56 @@ __device__ void q_mm(const QOp& o) {
   }
 }
 
+// reduce_sum / reduce_mean with r <= SF_CRO_CHUNK per output: the
+// canonical reduction order of sf_reduce.cu — lane l folds elements l,
+// l+32, ... left to right, then the xor butterfly combines the lanes present
+// — one warp per output; mean divides in the dtype (reduce_finalize).
+// shape/st[0]: kept dims; st[1]/st[2]: reduced extents/strides.
+template <class T>
+__device__ void q_reduce(const QOp& o) {
+  const T* in = (const T*)o.in[0];
+  T* out = (T*)o.out;
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int r = o.mm;
+  for (int w = threadIdx.x >> 5; w < o.n; w += warps) {
+    int rem = w, base = 0;
+#pragma unroll
+    for (int d = kQueueDims - 1; d >= 0; --d) {
+      if (d < o.ndim) {
+        const int e = o.shape[d];
+        base += (rem % e) * o.st[0][d];
+        rem /= e;
+      }
+    }
+    T acc = T(0);
+    bool present = false;
+    for (int j = lane; j < r; j += 32) {
+      int jr = j, off = 0;
+#pragma unroll
+      for (int d = kQueueDims - 1; d >= 0; --d) {
+        if (d < o.n_in) {
+          const int e = o.st[1][d];
+          off += (jr % e) * o.st[2][d];
+          jr /= e;
+        }
+      }
+      const T v = in[base + off];
+      acc = present ? acc + v : v;
+      present = true;
+    }
+#pragma unroll
+    for (int sh = 16; sh >= 1; sh >>= 1) {
+      const T ov = __shfl_xor_sync(0xffffffffu, acc, sh);
+      const bool op = __shfl_xor_sync(0xffffffffu, present, sh);
+      if (present && op) acc = acc + ov;
+      else if (op) acc = ov;
+      present = present || op;
+    }
+    if (lane == 0) out[w] = o.op ? acc / (T)r : acc;
+  }
+}
+
 __device__ __forceinline__ bool q_to_bool(int op) {
   return op == SF_OP_GREATER || op == SF_OP_LESS || op == SF_OP_EQUAL ||
          op == SF_OP_GREATER_EQUAL || op == SF_OP_ISFINITE;
@@ -120,6 +170,11 @@ __device__ void q_run(const QOp& o) {
   if (o.kind == SF_QOP_MATMUL) {
     if (o.dtype == SF_DTYPE_F64) q_mm<double>(o);
     else q_mm<float>(o);
+    return;
+  }
+  if (o.kind == SF_QOP_REDUCE) {
+    if (o.dtype == SF_DTYPE_F64) q_reduce<double>(o);
+    else q_reduce<float>(o);
     return;
   }
   const bool tb = q_to_bool(o.op);
@@ -251,7 +306,38 @@ static bool out_is_bool(int op) {
          op == SF_OP_GREATER_EQUAL || op == SF_OP_ISFINITE || op == SF_OP_LOGICAL_NOT;
 }
 
+static bool compact_reduce(const Device* d, const sf_op_desc& s, QOp* o) {
+  if ((s.dtype != SF_DTYPE_F32 && s.dtype != SF_DTYPE_F64) || s.ndim < 0 || s.ndim > SF_MAX_DIMS)
+    return false;
+  long long total = 1;
+  for (int i = 0; i < s.ndim; ++i) total *= s.shape[i];
+  if (total <= 0 || total > d->q_max_numel) return false;
+  RedGeom g;
+  reduce_geometry(s.ndim, s.shape, (uint32_t)s.m, &g);
+  if (g.r > SF_CRO_CHUNK || g.kept_nd > kQueueDims || g.red_nd > kQueueDims) return false;
+  std::memset(o, 0, sizeof(QOp));
+  o->kind = SF_QOP_REDUCE;
+  o->op = s.op ? 1 : 0;
+  o->dtype = s.dtype;
+  o->ndim = g.kept_nd;
+  o->n_in = g.red_nd;
+  o->n = (int)g.n_out;
+  o->mm = (int)g.r;
+  for (int i = 0; i < g.kept_nd; ++i) {
+    o->shape[i] = (int)g.kept_shape[i];
+    o->st[0][i] = (int)g.kept_stride[i];
+  }
+  for (int i = 0; i < g.red_nd; ++i) {
+    o->st[1][i] = (int)g.red_shape[i];
+    o->st[2][i] = (int)g.red_stride[i];
+  }
+  o->in[0] = s.in[0];
+  return true;
+}
+
 static int direct_launch(Device* d, const sf_op_desc& s, void* out) {
+  if (s.kind == SF_QOP_REDUCE)
+    return launch_reduce(d, s.op, s.dtype, s.ndim, s.shape, (uint32_t)s.m, s.in[0], out);
   if (s.kind == SF_QOP_MATMUL)
     return launch_matmul(d, s.dtype, s.m, s.n, s.k, s.in[0], s.op & 1, s.in[1], (s.op >> 1) & 1,
                          out);
@@ -283,6 +369,8 @@ int queue_submit(Device* d, const sf_op_desc& s, void* out) {
       }
     } else if (s.kind == SF_QOP_EW) {
       fits = compact_ew(d, s, &o);
+    } else if (s.kind == SF_QOP_REDUCE) {
+      fits = compact_reduce(d, s, &o);
     }
   }
   if (!fits) {
@@ -333,6 +421,15 @@ int sf_queue_push(int dev, const sf_op_desc* desc, void** out) {
     for (int i = 0; i < s.ndim; ++i) n *= s.shape[i];
     const int odt = s.op == SF_OP_SELECT ? s.dtype : (out_is_bool(s.op) ? SF_DTYPE_BOOL : s.dtype);
     bytes = (size_t)n * dtype_size(odt);
+  } else if (s.kind == SF_QOP_REDUCE) {
+    if (s.ndim < 0 || s.ndim > SF_MAX_DIMS) {
+      set_error("sf_queue_push: bad reduction rank");
+      return SF_ERR_INVALID;
+    }
+    long long n_out = 1;
+    for (int i = 0; i < s.ndim; ++i)
+      if (!((uint32_t)s.m & (1u << i))) n_out *= s.shape[i];
+    bytes = (size_t)n_out * dtype_size(s.dtype);
   } else {
     set_error("sf_queue_push: unknown op kind");
     return SF_ERR_INVALID;

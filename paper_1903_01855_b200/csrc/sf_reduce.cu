@@ -474,42 +474,58 @@ static int run_reduce(Device* d, const RedArgs& a, const T* in, A* sums) {
   return SF_OK;
 }
 
-int launch_reduce(Device* d, int op, int dtype, int ndim, const int64_t* shape,
-                  uint32_t axes_mask, const void* in, void* out) {
-  RedArgs a;
-  std::memset(&a, 0, sizeof(a));
+void reduce_geometry(int ndim, const int64_t* shape, uint32_t axes_mask, RedGeom* g) {
+  std::memset(g, 0, sizeof(*g));
   long long stride[SF_MAX_DIMS];
   long long s = 1;
   for (int i = ndim - 1; i >= 0; --i) {
     stride[i] = s;
     s *= shape[i];
   }
-  a.n_out = 1;
-  a.r = 1;
+  g->n_out = 1;
+  g->r = 1;
   for (int i = 0; i < ndim; ++i) {
     if (shape[i] == 1) continue;  // size-1 dims do not affect either side
     if (axes_mask & (1u << i)) {
       // merge with the previous reduced dim if contiguous
-      if (a.red_nd > 0 && a.red_stride[a.red_nd - 1] == stride[i] * shape[i]) {
-        a.red_shape[a.red_nd - 1] *= shape[i];
-        a.red_stride[a.red_nd - 1] = stride[i];
+      if (g->red_nd > 0 && g->red_stride[g->red_nd - 1] == stride[i] * shape[i]) {
+        g->red_shape[g->red_nd - 1] *= shape[i];
+        g->red_stride[g->red_nd - 1] = stride[i];
       } else {
-        a.red_shape[a.red_nd] = shape[i];
-        a.red_stride[a.red_nd] = stride[i];
-        ++a.red_nd;
+        g->red_shape[g->red_nd] = shape[i];
+        g->red_stride[g->red_nd] = stride[i];
+        ++g->red_nd;
       }
-      a.r *= shape[i];
+      g->r *= shape[i];
     } else {
-      if (a.kept_nd > 0 && a.kept_stride[a.kept_nd - 1] == stride[i] * shape[i]) {
-        a.kept_shape[a.kept_nd - 1] *= shape[i];
-        a.kept_stride[a.kept_nd - 1] = stride[i];
+      if (g->kept_nd > 0 && g->kept_stride[g->kept_nd - 1] == stride[i] * shape[i]) {
+        g->kept_shape[g->kept_nd - 1] *= shape[i];
+        g->kept_stride[g->kept_nd - 1] = stride[i];
       } else {
-        a.kept_shape[a.kept_nd] = shape[i];
-        a.kept_stride[a.kept_nd] = stride[i];
-        ++a.kept_nd;
+        g->kept_shape[g->kept_nd] = shape[i];
+        g->kept_stride[g->kept_nd] = stride[i];
+        ++g->kept_nd;
       }
-      a.n_out *= shape[i];
+      g->n_out *= shape[i];
     }
+  }
+}
+
+int launch_reduce(Device* d, int op, int dtype, int ndim, const int64_t* shape,
+                  uint32_t axes_mask, const void* in, void* out) {
+  RedArgs a;
+  std::memset(&a, 0, sizeof(a));
+  RedGeom g;
+  reduce_geometry(ndim, shape, axes_mask, &g);
+  a.n_out = g.n_out;
+  a.r = g.r;
+  a.kept_nd = g.kept_nd;
+  a.red_nd = g.red_nd;
+  for (int i = 0; i < SF_MAX_DIMS; ++i) {
+    a.kept_shape[i] = g.kept_shape[i];
+    a.kept_stride[i] = g.kept_stride[i];
+    a.red_shape[i] = g.red_shape[i];
+    a.red_stride[i] = g.red_stride[i];
   }
   long long total = 1;
   for (int i = 0; i < ndim; ++i) total *= shape[i];
@@ -585,12 +601,27 @@ using namespace sfrt;
 
 extern "C" int sf_reduce(int dev, int op, int dtype, int ndim, const int64_t* shape,
                          uint32_t axes_mask, const void* in, void** out) {
-  Device* d;
-  SF_TRY(ensure_device(dev, &d));
   if (ndim < 0 || ndim > SF_MAX_DIMS) {
     set_error("sf_reduce: bad rank");
     return SF_ERR_INVALID;
   }
+  // short float reductions (one CRO chunk per output) go through the launch
+  // queue, which evaluates the same CRO tree (sf_queue.cu)
+  if (dtype == SF_DTYPE_F32 || dtype == SF_DTYPE_F64) {
+    sf_op_desc q;
+    std::memset(&q, 0, sizeof(q));
+    q.kind = SF_QOP_REDUCE;
+    q.op = op;
+    q.dtype = dtype;
+    q.ndim = ndim;
+    q.n_in = 1;
+    q.m = axes_mask;
+    q.in[0] = in;
+    for (int i = 0; i < ndim; ++i) q.shape[i] = shape[i];
+    return sf_queue_push(dev, &q, out);
+  }
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
   long long n_out = 1;
   for (int i = 0; i < ndim; ++i)
     if (!(axes_mask & (1u << i))) n_out *= shape[i];
