@@ -574,7 +574,7 @@ def extras(sf, np, _native, plugins, l2hmc):
                 continue
             sf.init_runtime(sf.RuntimeOptions())
             wl = Leapfrog(b, mode)
-            dt = _time_steps(wl.step, 50 if mode == "staged" else 3, _native)
+            dt = _time_steps(wl.step, 50 if mode == "staged" else 10, _native)
             row[mode] = {"chains_per_sec": b / dt, "us_per_trajectory": dt * 1e6}
         if "eager" in row:
             row["staged_over_eager"] = row["staged"]["chains_per_sec"] / row["eager"]["chains_per_sec"]
@@ -583,7 +583,7 @@ def extras(sf, np, _native, plugins, l2hmc):
     out["leapfrog"] = lf
     # C2 microbenchmark: 100 x (matmul + add + tanh), primitive ops/s
     c2 = {}
-    for mode, n in (("staged", 50), ("eager", 3)):
+    for mode, n in (("staged", 50), ("eager", 20)):
         sf.init_runtime(sf.RuntimeOptions())
         plugins.install()
         mb = microbench.Chain(mode)
@@ -591,12 +591,46 @@ def extras(sf, np, _native, plugins, l2hmc):
         c2[mode] = {"ops_per_sec": 300 / dt, "us_per_op": dt * 1e6 / 300}
     c2["staged_over_eager"] = c2["staged"]["ops_per_sec"] / c2["eager"]["ops_per_sec"]
     out["c2_microbench"] = c2
+    out["eager_launch_path"] = eager_path_extra(sf, np, _native, plugins)
     out["c4_resnet50_b32"] = resnet_extra(sf, np, _native)
     try:
         out["c5_resnet50_b256_1gpu"] = c5_extra(sf, _native, 0, 1, None)
     except Exception as e:  # report, never lose the headline line
         out["c5_resnet50_b256_1gpu"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     out["f1_device_while"] = while_extra(sf, np, _native)
+    return out
+
+
+def eager_path_extra(sf, np, _native, plugins):
+    """North-star subsystem 1, the eager launch path: host+device cost per
+    primitive (wall clock over 20k dispatches incl. the final sync) through
+    the native front-end + launch queue (default), the native front-end with
+    one kernel launch per op, and the reference-semantics Python dispatcher
+    (ops._dispatch_py) with one launch per op; plus kernel launches per op."""
+    from paper_1903_01855_b200 import _fastpath
+    from paper_1903_01855_b200.workloads import microbench
+
+    out = {}
+    sf.init_runtime(sf.RuntimeOptions())
+    plugins.install()
+    x = sf.constant(np.ones((1, 16), np.float32))
+    for mode in ("queue", "direct", "python"):
+        _fastpath.set_enabled(mode != "python")
+        _native.queue_config(0, 64 if mode == "queue" else 0)
+        n = 20000
+        l0 = _native.launch_count(0)
+        add_us = _time_steps(lambda: sf.add(x, x), n, _native) * 1e6
+        launches = (_native.launch_count(0) - l0) / (n + 2)
+        ch = microbench.Chain("eager")
+        c2_us = _time_steps(ch.step, 20, _native) * 1e6 / 300
+        out[mode] = {"add_us_per_op": add_us, "kernel_launches_per_op": launches,
+                     "c2_eager_us_per_op": c2_us}
+    _fastpath.set_enabled(True)
+    _native.queue_config(0, 64)
+    out["what"] = ("eager sf.add on (1,16) f32 and the C2 eager chain; queue = native "
+                   "front-end + launch queue (64 ops per interpreter-kernel launch), direct = "
+                   "native front-end with one launch per op, python = reference-semantics "
+                   "Python dispatcher with one launch per op")
     return out
 
 
