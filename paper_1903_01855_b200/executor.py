@@ -126,9 +126,14 @@ class Program:
         self.keep: List = []  # constant tensors whose buffers plans point at
         lw = Lowerer(self.dev, rng_mode)
         self.in_vals: List[LV] = []
+        # inputs the program is specialised on (index -> weakref of the tensor)
+        self.baked: Dict[int, "weakref.ref"] = {}
         for i, (ph, v) in enumerate(zip(gf.inputs, inputs)):
             lv = lw.new(v.dtype, v.shape, "var" if ph.is_variable_ref else "input")
             lv.index = i
+            if fuse_enabled and bakeable(ph, v):
+                lv.vals = v.raw().reshape(-1)
+                self.baked[i] = weakref.ref(v)
             self.in_vals.append(lv)
         self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)
         from . import rowfuse
@@ -599,8 +604,31 @@ class Program:
             env[id(lv)] = t
 
 
+# Small immutable tensors a staged function captured (network weights, masks)
+# are specialised into the generated row kernels as literal operands: an
+# FFMA with an immediate weight instead of a shared-memory load per use
+# (the L2HMC row kernel was bound by shared-memory load latency and the LSU
+# pipe, profiles/r02c_l2hmc_rows_full.md).  The compiled program is keyed by
+# the identity of those tensors (tensors are immutable; a capture of a trace
+# is the same object on every call).  SF_BAKE=0 disables it.
+BAKE = __import__("os").environ.get("SF_BAKE", "1") == "1"
+BAKE_MAX_NUMEL = 1024
+# tensors captured by a ConcreteFunction (staging.py): the same immutable
+# object is passed on every call of that function
+STABLE_CAPTURES: "weakref.WeakSet" = weakref.WeakSet()
+
+
+def bakeable(ph, v) -> bool:
+    return (BAKE and not ph.is_variable_ref and isinstance(v, Tensor) and v._symbolic is None
+            and v.dtype.is_float and 0 < v.size <= BAKE_MAX_NUMEL and v in STABLE_CAPTURES)
+
+
 def _signature(inputs: Sequence) -> Tuple:
     return tuple((type(v).__name__ == "Variable", v.dtype, v.shape) for v in inputs)
+
+
+def _bake_key(gf: GraphFunction, inputs: Sequence) -> Tuple:
+    return tuple(id(v) for ph, v in zip(gf.inputs, inputs) if bakeable(ph, v))
 
 
 def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
@@ -618,16 +646,19 @@ def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
     last = gf.__dict__.get("_last_prog")
     if last is not None and last[0] == pkey and len(last[1]) == len(inputs):
         refs, comps, prog = last[1], last[2], last[3]
+        baked = prog.baked
         for i, v in enumerate(inputs):
             if refs[i]() is v:
                 continue
-            if (type(v).__name__ == "Variable", v.dtype, v.shape) != comps[i]:
+            if i in baked or (type(v).__name__ == "Variable", v.dtype, v.shape) != comps[i]:
                 break
             refs[i] = weakref.ref(v)
         else:
             return prog
-    key = (pkey, _signature(inputs))
+    key = (pkey, _signature(inputs), _bake_key(gf, inputs))
     prog = cache.get(key)
+    if prog is not None and any(r() is not inputs[i] for i, r in prog.baked.items()):
+        prog = None  # an id reused by a different tensor
     if prog is None:
         if any(k[0][1] != rt.generation for k in cache):
             cache.clear()  # programs of a replaced runtime

@@ -39,7 +39,8 @@ from .tensor import Tensor
 class LV:
     """A lowered value.  kinds: input, var, const, op, alias."""
 
-    __slots__ = ("id", "dtype", "shape", "kind", "index", "tensor", "base", "imm", "producer")
+    __slots__ = ("id", "dtype", "shape", "kind", "index", "tensor", "base", "imm", "producer",
+                 "vals")
 
     def __init__(self, id_, dtype: DType, shape, kind: str):
         self.id = id_
@@ -51,6 +52,9 @@ class LV:
         self.base = None      # alias target
         self.imm = None       # scalar literal if the value is a known splat
         self.producer = None  # LOp
+        # host values of an immutable captured tensor the program is
+        # specialised on (row kernels read its elements as literals)
+        self.vals = None
 
     @property
     def numel(self) -> int:

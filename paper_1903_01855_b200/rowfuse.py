@@ -639,8 +639,8 @@ class _Gen:
                 r = b.root()
                 if planner.layout_of(b)[0] == ROW or id(r) in self.produced:
                     continue
-                if r.kind == "const" and r.imm is not None:
-                    continue
+                if (r.kind == "const" and r.imm is not None) or r.vals is not None:
+                    continue  # literal weights: scalar FMAs with immediates
                 n = b.shape[1]
                 prev = seen.get(id(r))
                 seen[id(r)] = n if prev in (None, n) else False
@@ -672,6 +672,9 @@ class _Gen:
         r = x.root()
         if id(r) in self.produced or (r.kind == "const" and r.imm is not None):
             return
+        if (r.vals is not None and not self.rp.uniform_only
+                and self.P.layout_of(x)[0] == UNI):
+            return  # specialised immutable capture: read as literals (uni_elem)
         if id(r) in self.ptr_of:
             k = self.ptr_of[id(r)]
             if (self.P.layout_of(x)[0] == UNI and not self.rp.uniform_only
@@ -829,6 +832,8 @@ class _Gen:
         r = x.root()
         if r.kind == "const" and r.imm is not None:
             return c_literal(r.imm, r.dtype)
+        if r.vals is not None and id(r) not in self.uni_names:
+            return c_literal(r.vals[flat].item(), r.dtype)
         names = self.uni_names[id(r)]
         return names[flat]
 

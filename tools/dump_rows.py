@@ -77,12 +77,16 @@ def main():
         args = [s.x] if draws == "runtime" else [s.x] + [
             sf.tensor_from_host(d.reshape(-1), d.shape, sf.float32) for d in s.host_draws()]
         pf = s.transition
-    gf = pf._concrete_for(pf._bind(tuple(args), {})).graph
+    cf = pf._concrete_for(pf._bind(tuple(args), {}))
+    gf = cf.graph
     lw = Lowerer(0, "device")
     ins = []
-    for i, (ph, v) in enumerate(zip(gf.inputs, args + [None] * len(gf.inputs))):
+    values = list(args) + cf.materialize_captured()
+    for i, (ph, v) in enumerate(zip(gf.inputs, values)):
         lv = lw.new(ph.dtype, ph.shape, "var" if ph.is_variable_ref else "input")
         lv.index = i
+        if executor.bakeable(ph, v):  # as Program does
+            lv.vals = v.raw().reshape(-1)
         ins.append(lv)
     outs = lw.lower_graph(gf, ins, ())
     ops = cse(lw.ops)
