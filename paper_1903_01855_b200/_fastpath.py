@@ -156,6 +156,8 @@ def configure(rt) -> None:
         spec = fast_spec(d)
         if spec is not None:
             fast.append((d.name, d) + tuple(spec))
+        elif d.name == "call_function":
+            fast.append((d.name, d, 0, 0, 0))  # counted by the staged-call path
     dev = rt.devices[0]
     # (no GPU: the fast path stays off and the Python path reports it)
     single = len(rt.devices) == 1 and rt.backend_available
@@ -203,3 +205,40 @@ def set_enabled(on: bool) -> bool:
     """Enable/disable the native fast path (tests compare both); returns the
     previous state."""
     return ext.set_enabled(on) if NATIVE else False
+
+
+def staged_fast(rt, cf, prog, args, structure: str):
+    """The native repeat-call path of a staged function (ext.StagedFast) for
+    calls like `args` (positional tensors), or None when the program is not
+    one native plan or a capture is not a plain tensor."""
+    if not NATIVE or len(rt.devices) != 1 or not rt.backend_available:
+        return None
+    from .tensor import Tensor
+
+    fast = prog._single_plan() if prog.__dict__.get("_fast") is None else prog._fast
+    if not fast or prog.__dict__.get("_replay"):
+        return None
+    plan, pos, specs = fast
+    caps = cf.materialize_captured()
+    everything = list(args) + caps
+    if not all(type(v) is Tensor for v in everything):
+        return None
+    n_args = len(args)
+    in_src, in_ptr = [], []
+    for i in pos:
+        if i < n_args:
+            in_src.append(i)
+            in_ptr.append(0)
+        else:
+            in_src.append(-1)
+            in_ptr.append(everything[i]._ptr())
+    code = {"none": 0, "single": 1, "tuple": 2, "list": 3}[structure]
+    return ext.StagedFast(rt, (prog, plan, tuple(caps), cf), plan._lock, plan.handle, prog.dev,
+                          prog.device, tuple(a.dtype for a in args),
+                          tuple(a.shape for a in args), in_src, in_ptr,
+                          [j for j, _, _, _ in specs], [nb for _, nb, _, _ in specs],
+                          tuple(dt for _, _, dt, _ in specs),
+                          tuple(tuple(sh) for _, _, _, sh in specs), code)
+
+
+MISS = ext.MISS if NATIVE else object()

@@ -1053,6 +1053,229 @@ PyObject* T_richcompare(PyObject* a, PyObject* b, int op) {
 
 PyNumberMethods Tensor_number = {};
 
+// ------------------------------------------------------- staged call path
+//
+// StagedFast: the repeat-call fast path of one staged function (reference:
+// PolymorphicFunction.__call__ -> call_concrete -> dispatch("call_function")
+// -> execute_graph, stageflow/staging.py:453-460, :353-407,
+// stageflow/kernels.py:460-480).  Built by staging.py after a call that
+// took the slow path, for a function whose program is one native plan and
+// whose captures are all tensors.  A call with the same number of
+// positional tensor arguments of the same dtypes and shapes (the same trace
+// key) runs the plan directly: argument pointers plus the captures'
+// pre-resolved pointers, one sf_plan_run, output tensors built here, the
+// call_function dispatch counted.  Anything else returns MISS and the
+// caller runs the reference path.
+
+PyObject* g_miss = nullptr;
+unsigned long long g_graph_launches = 0;
+int g_call_idx = -1;  // table index of "call_function" (its eager counter)
+
+struct StagedFast {
+  PyObject_HEAD
+  PyObject* rt;
+  PyObject* keep;        // objects kept alive (program, plan, captures)
+  PyObject* lock;        // the plan's Python lock (shared with Plan.run)
+  PyObject* arg_dtypes;  // tuple
+  PyObject* arg_shapes;  // tuple
+  PyObject* out_dtypes;  // tuple
+  PyObject* out_shapes;  // tuple
+  PyObject* device;
+  void* plan;
+  int dev, n_args, n_in, n_out, structure;
+  int* in_src;           // plan input -> explicit arg index, or -1 (capture)
+  void** in_ptr;         // capture pointers pre-filled
+  int* out_slot;
+  Py_ssize_t* out_nbytes;
+  vectorcallfunc vectorcall;
+};
+
+PyObject* StagedFast_call(PyObject* o, PyObject* const* args, size_t nargsf, PyObject* kw) {
+  StagedFast* f = (StagedFast*)o;
+  const Py_ssize_t n = PyVectorcall_NARGS(nargsf);
+  if (kw || n != f->n_args) return Py_NewRef(g_miss);
+  PyObject* ctx = fast_context();
+  if (!ctx || f->rt != g_rt || tapes_active(ctx)) {
+    if (PyErr_Occurred()) return nullptr;
+    return Py_NewRef(g_miss);
+  }
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* a = args[i];
+    if (!is_tensor(a) || !concrete(a)) return Py_NewRef(g_miss);
+    TensorObj* t = (TensorObj*)a;
+    if (t->dtype != PyTuple_GET_ITEM(f->arg_dtypes, i)) return Py_NewRef(g_miss);
+    PyObject* want = PyTuple_GET_ITEM(f->arg_shapes, i);
+    if (t->shape != want) {
+      const int eq = PyObject_RichCompareBool(t->shape, want, Py_EQ);
+      if (eq < 0) return nullptr;
+      if (!eq) return Py_NewRef(g_miss);
+    }
+  }
+  void* ins[256];
+  void* outs[256];
+  for (int k = 0; k < f->n_in; ++k) {
+    const int src = f->in_src[k];
+    if (src < 0) {
+      ins[k] = f->in_ptr[k];
+    } else {
+      const void* p;
+      if (!device_ptr((TensorObj*)args[src], &p)) return nullptr;
+      ins[k] = (void*)p;
+    }
+  }
+  // serialise with Plan.run on the same plan (non-blocking: busy -> MISS)
+  PyObject* got = PyObject_CallMethod(f->lock, "acquire", "O", Py_False);
+  if (!got) return nullptr;
+  const int have = PyObject_IsTrue(got);
+  Py_DECREF(got);
+  if (have != 1) return Py_NewRef(g_miss);
+  const int st = sf_plan_run(f->plan, ins, outs);
+  PyObject* rel = PyObject_CallMethod(f->lock, "release", nullptr);
+  Py_XDECREF(rel);
+  if (st != SF_OK) return kernel_error("plan run");
+  PyObject* res = PyTuple_New(f->n_out);
+  if (!res) return nullptr;
+  for (int j = 0; j < f->n_out; ++j) {
+    PyObject* buf = new_devbuf(f->dev, outs[f->out_slot[j]], f->out_nbytes[j]);
+    PyObject* t = buf ? new_tensor(PyTuple_GET_ITEM(f->out_dtypes, j),
+                                   PyTuple_GET_ITEM(f->out_shapes, j), buf, nullptr)
+                      : nullptr;
+    Py_XDECREF(buf);
+    if (!t) {
+      Py_DECREF(res);
+      return nullptr;
+    }
+    PyTuple_SET_ITEM(res, j, t);
+  }
+  if (f->n_out > 1) {  // siblings: reading one output enqueues the others' reads
+    PyObject* sib = PyList_New(f->n_out);
+    if (!sib) {
+      Py_DECREF(res);
+      return nullptr;
+    }
+    for (int j = 0; j < f->n_out; ++j) {
+      PyObject* w = PyWeakref_NewRef(PyTuple_GET_ITEM(res, j), nullptr);
+      if (!w) {
+        Py_DECREF(sib);
+        Py_DECREF(res);
+        return nullptr;
+      }
+      PyList_SET_ITEM(sib, j, w);
+    }
+    for (int j = 0; j < f->n_out; ++j) {
+      TensorObj* t = (TensorObj*)PyTuple_GET_ITEM(res, j);
+      Py_XSETREF(t->sib, Py_NewRef(sib));
+    }
+    Py_DECREF(sib);
+  }
+  if (g_call_idx >= 0) g_ops[g_call_idx].count++;
+  g_graph_launches++;
+  switch (f->structure) {
+    case 0:
+      Py_DECREF(res);
+      Py_RETURN_NONE;
+    case 1: {
+      PyObject* one = Py_NewRef(PyTuple_GET_ITEM(res, 0));
+      Py_DECREF(res);
+      return one;
+    }
+    case 2:
+      return res;
+    default: {
+      PyObject* lst = PySequence_List(res);
+      Py_DECREF(res);
+      return lst;
+    }
+  }
+}
+
+void StagedFast_dealloc(PyObject* o) {
+  StagedFast* f = (StagedFast*)o;
+  PyObject_GC_UnTrack(o);
+  Py_CLEAR(f->rt);
+  Py_CLEAR(f->keep);
+  Py_CLEAR(f->lock);
+  Py_CLEAR(f->arg_dtypes);
+  Py_CLEAR(f->arg_shapes);
+  Py_CLEAR(f->out_dtypes);
+  Py_CLEAR(f->out_shapes);
+  Py_CLEAR(f->device);
+  PyMem_Free(f->in_src);
+  PyMem_Free(f->in_ptr);
+  PyMem_Free(f->out_slot);
+  PyMem_Free(f->out_nbytes);
+  Py_TYPE(o)->tp_free(o);
+}
+
+int StagedFast_traverse(PyObject* o, visitproc visit, void* arg) {
+  StagedFast* f = (StagedFast*)o;
+  Py_VISIT(f->rt);
+  Py_VISIT(f->keep);
+  Py_VISIT(f->lock);
+  return 0;
+}
+
+// StagedFast(rt, keep, lock, plan_handle, dev, device, arg_dtypes, arg_shapes,
+//            in_src (list: arg index or -1), in_ptr (list: capture pointer or 0),
+//            out_slots, out_nbytes, out_dtypes, out_shapes, structure)
+PyObject* StagedFast_new(PyTypeObject* type, PyObject* args, PyObject*) {
+  PyObject *rt, *keep, *lock, *device, *adt, *ash, *isrc, *iptr, *oslot, *onb, *odt, *osh;
+  unsigned long long plan;
+  int dev, structure;
+  if (!PyArg_ParseTuple(args, "OOOKiOO!O!O!O!O!O!O!O!i", &rt, &keep, &lock, &plan, &dev,
+                        &device, &PyTuple_Type, &adt, &PyTuple_Type, &ash, &PyList_Type, &isrc,
+                        &PyList_Type, &iptr, &PyList_Type, &oslot, &PyList_Type, &onb,
+                        &PyTuple_Type, &odt, &PyTuple_Type, &osh, &structure))
+    return nullptr;
+  const Py_ssize_t n_in = PyList_GET_SIZE(isrc), n_out = PyList_GET_SIZE(oslot);
+  if (n_in > 256 || n_out > 256 || PyList_GET_SIZE(iptr) != n_in ||
+      PyList_GET_SIZE(onb) != n_out || PyTuple_GET_SIZE(odt) != n_out ||
+      PyTuple_GET_SIZE(osh) != n_out || PyTuple_GET_SIZE(adt) != PyTuple_GET_SIZE(ash)) {
+    PyErr_SetString(PyExc_ValueError, "StagedFast: inconsistent arguments");
+    return nullptr;
+  }
+  StagedFast* f = (StagedFast*)type->tp_alloc(type, 0);
+  if (!f) return nullptr;
+  f->rt = Py_NewRef(rt);
+  f->keep = Py_NewRef(keep);
+  f->lock = Py_NewRef(lock);
+  f->arg_dtypes = Py_NewRef(adt);
+  f->arg_shapes = Py_NewRef(ash);
+  f->out_dtypes = Py_NewRef(odt);
+  f->out_shapes = Py_NewRef(osh);
+  f->device = Py_NewRef(device);
+  f->plan = (void*)(uintptr_t)plan;
+  f->dev = dev;
+  f->n_args = (int)PyTuple_GET_SIZE(adt);
+  f->n_in = (int)n_in;
+  f->n_out = (int)n_out;
+  f->structure = structure;
+  f->in_src = (int*)PyMem_Calloc(n_in + 1, sizeof(int));
+  f->in_ptr = (void**)PyMem_Calloc(n_in + 1, sizeof(void*));
+  f->out_slot = (int*)PyMem_Calloc(n_out + 1, sizeof(int));
+  f->out_nbytes = (Py_ssize_t*)PyMem_Calloc(n_out + 1, sizeof(Py_ssize_t));
+  f->vectorcall = StagedFast_call;
+  if (!f->in_src || !f->in_ptr || !f->out_slot || !f->out_nbytes) {
+    Py_DECREF(f);
+    return PyErr_NoMemory();
+  }
+  for (Py_ssize_t k = 0; k < n_in; ++k) {
+    f->in_src[k] = (int)PyLong_AsLong(PyList_GET_ITEM(isrc, k));
+    f->in_ptr[k] = PyLong_AsVoidPtr(PyList_GET_ITEM(iptr, k));
+  }
+  for (Py_ssize_t j = 0; j < n_out; ++j) {
+    f->out_slot[j] = (int)PyLong_AsLong(PyList_GET_ITEM(oslot, j));
+    f->out_nbytes[j] = PyLong_AsSsize_t(PyList_GET_ITEM(onb, j));
+  }
+  if (PyErr_Occurred()) {
+    Py_DECREF(f);
+    return nullptr;
+  }
+  return (PyObject*)f;
+}
+
+PyTypeObject StagedFastType = {PyVarObject_HEAD_INIT(nullptr, 0)};
+
 // ---------------------------------------------------------- configuration
 
 // bootstrap(rt_module_dict, thread_local, configure_cb, slow_dispatch,
@@ -1153,6 +1376,10 @@ PyObject* py_configure(PyObject*, PyObject* args) {
   off_scopes = os;
   g_single = single != 0;
   g_ordinal = ordinal;
+  g_call_idx = -1;
+  for (int i = 0; i < g_nops; ++i)
+    if (PyUnicode_CompareWithASCIIString(g_ops[i].name, "call_function") == 0) g_call_idx = i;
+  g_graph_launches = 0;
   Py_RETURN_NONE;
 }
 
@@ -1186,6 +1413,16 @@ PyObject* py_add_op(PyObject*, PyObject* args) {
 PyObject* py_drain(PyObject*, PyObject* rt) {
   PyObject* d = PyDict_New();
   if (!d || rt != g_rt) return d;
+  if (g_graph_launches) {
+    PyObject* v = PyLong_FromUnsignedLongLong(g_graph_launches);
+    if (!v || PyDict_SetItemString(d, "<graph_launches>", v) < 0) {
+      Py_XDECREF(v);
+      Py_DECREF(d);
+      return nullptr;
+    }
+    Py_DECREF(v);
+    g_graph_launches = 0;
+  }
   for (int i = 0; i < g_nops; ++i) {
     if (!g_ops[i].count) continue;
     PyObject* v = PyLong_FromUnsignedLongLong(g_ops[i].count);
@@ -1288,11 +1525,26 @@ PyMODINIT_FUNC PyInit__sfeager(void) {
   FastWrapperType.tp_members = FastWrapper_members;
   if (PyType_Ready(&FastWrapperType) < 0) return nullptr;
 
+  StagedFastType.tp_name = "_sfeager.StagedFast";
+  StagedFastType.tp_doc = "Repeat-call fast path of one staged function.";
+  StagedFastType.tp_basicsize = sizeof(StagedFast);
+  StagedFastType.tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_HAVE_GC | Py_TPFLAGS_HAVE_VECTORCALL;
+  StagedFastType.tp_new = StagedFast_new;
+  StagedFastType.tp_dealloc = StagedFast_dealloc;
+  StagedFastType.tp_traverse = StagedFast_traverse;
+  StagedFastType.tp_call = PyVectorcall_Call;
+  StagedFastType.tp_vectorcall_offset = offsetof(StagedFast, vectorcall);
+  if (PyType_Ready(&StagedFastType) < 0) return nullptr;
+  g_miss = PyObject_CallNoArgs((PyObject*)&PyBaseObject_Type);
+  if (!g_miss) return nullptr;
+
   PyObject* m = PyModule_Create(&moddef);
   if (!m) return nullptr;
   if (PyModule_AddObjectRef(m, "DeviceBuffer", (PyObject*)&DevBufType) < 0 ||
       PyModule_AddObjectRef(m, "TensorBase", (PyObject*)&TensorBaseType) < 0 ||
       PyModule_AddObjectRef(m, "FastWrapper", (PyObject*)&FastWrapperType) < 0 ||
+      PyModule_AddObjectRef(m, "StagedFast", (PyObject*)&StagedFastType) < 0 ||
+      PyModule_AddObjectRef(m, "MISS", g_miss) < 0 ||
       PyModule_AddIntConstant(m, "K_EW1", K_EW1) < 0 ||
       PyModule_AddIntConstant(m, "K_EW2", K_EW2) < 0 ||
       PyModule_AddIntConstant(m, "K_MATMUL", K_MATMUL) < 0 ||

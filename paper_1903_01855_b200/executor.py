@@ -332,7 +332,7 @@ class Program:
         in_slots = [use(r) for r in ext]
         out_slots = [define(o) for o in outs]
         rows = rp.batch
-        per_cta = 128 * rp.replicas  # rp.replicas chains per thread
+        per_cta = rp.rows_per_cta  # 128 x replicas, or 64 for a team-split kernel
         grid = 1 if rp.uniform_only else max(1, (rows + per_cta - 1) // per_cta)
         ptrs = in_slots + out_slots
         n_rng = max(1, len(rng_counts))

@@ -98,7 +98,8 @@ REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 
 class RowProgram:
-    __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas", "cpool")
+    __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas", "cpool", "teams",
+                 "rows_per_cta")
 
     def __init__(self, batch: int):
         self.ops: List[LOp] = []
@@ -111,6 +112,10 @@ class RowProgram:
         self.block = 128  # threads per CTA (set by code generation)
         # chains per thread: large batches take 2 (shared weight loads, 2x ILP)
         self.replicas = ROW_REPLICAS if ROW_REPLICAS else (2 if batch >= REPLICA_MIN_BATCH else 1)
+        # two teams of warps per CTA, each running one independent half of
+        # the program for the same 64 chains (find_teams), or None
+        self.teams = None
+        self.rows_per_cta = 128  # chains per CTA (set by code generation)
 
 
 class LoopOp:
@@ -540,6 +545,10 @@ def plan_rows(ops: List[LOp], keep=frozenset()) -> List:
                 body = RowProgram(u.batch)
                 body.ops = reroll(row_ops, planner, users, keep) if REROLL else row_ops
                 chunks = _split(body, planner)
+                if 0 < batch <= TEAM_MAX_BATCH:
+                    for c in chunks:
+                        if c.replicas == 1:
+                            c.teams = find_teams(c, planner)
                 if (all(_smem_bytes(c, planner) <= MAX_SMEM_BYTES for c in chunks)
                         and _uniform_smem(uni) <= MAX_SMEM_BYTES):
                     if uni.ops:
@@ -554,6 +563,125 @@ def plan_rows(ops: List[LOp], keep=frozenset()) -> List:
         else:
             out.append(u)
     return out
+
+
+# Team split (latency-bound batches): a row program whose per-chain work
+# falls into independent parts — the L2HMC transition's forward and backward
+# trajectories, joined only by the direction select and the MH step — runs
+# as two teams of warps per CTA over the same 64 chains, each team executing
+# one part; the values the join needs cross through shared memory after one
+# barrier.  One thread's serial latency per chain halves, which is what
+# bounds small batches (C1: 200 chains, ~60 us of dependent instructions).
+# Above TEAM_MAX_BATCH chains the GPU is full with one chain per thread and
+# the split would only add a second wave.
+TEAM_MAX_BATCH = int(__import__("os").environ.get("SF_TEAM_MAX_BATCH", "40000"))
+TEAM_MIN_SHARE = 0.25   # each team carries at least this share of the work
+TEAM_MAX_JOIN = 0.10    # at most this share of the work runs after the barrier
+DUP_MAX_COST = 32       # ops computed from inputs alone up to this cost are recomputed per team
+
+
+def _full_cost(op, planner) -> int:
+    if op.kind == "loop":
+        return op.m * sum(_op_cost(b, planner) for b in op.body)
+    return _op_cost(op, planner)
+
+
+def find_teams(rp: RowProgram, planner) -> Optional[Tuple[List[LOp], List[LOp], List[LOp],
+                                                            List[LV], List[LV]]]:
+    """(team 0 ops, team 1 ops, join ops, team-0 values the join reads,
+    team-1 values the join reads), or None when the program does not split."""
+    ops = rp.ops
+    n = len(ops)
+    if n < 4:
+        return None
+    prod: Dict[int, int] = {}
+    for i, op in enumerate(ops):
+        for o in op.outs:
+            prod[id(o)] = i
+    deps = [set() for _ in ops]
+    users = [set() for _ in ops]
+    for i, op in enumerate(ops):
+        for x in op.ins:
+            j = prod.get(id(x.root()))
+            if j is not None and j != i:
+                deps[i].add(j)
+                users[j].add(i)
+    cost = [_full_cost(op, planner) for op in ops]
+    total = float(sum(cost)) or 1.0
+    # cheap ops computed from the program's inputs alone (random draws, the
+    # energy and force at the initial state both trajectories start from) are
+    # recomputed by every part that uses them instead of linking the parts
+    dup = [False] * n
+    for i, op in enumerate(ops):
+        dup[i] = (op.kind != "loop" and (op.kind == "rng" or cost[i] <= DUP_MAX_COST)
+                  and all(dup[j] for j in deps[i]))
+    rest = {i for i in range(n) if not dup[i]}
+    join: set = set()
+
+    def parts():
+        parent = {i: i for i in rest}
+
+        def find(i):
+            while parent[i] != i:
+                parent[i] = parent[parent[i]]
+                i = parent[i]
+            return i
+
+        for i in rest:
+            for j in deps[i]:
+                if j in rest:
+                    parent[find(i)] = find(j)
+        groups: Dict[int, List[int]] = {}
+        for i in rest:
+            groups.setdefault(find(i), []).append(i)
+        return list(groups.values())
+
+    while True:
+        comps = parts()
+        if len(comps) >= 2:
+            comps.sort(key=lambda g: -sum(cost[i] for i in g))
+            sides = [[], []]
+            load = [0, 0]
+            for g in comps:
+                t = 0 if load[0] <= load[1] else 1
+                sides[t] += g
+                load[t] += sum(cost[i] for i in g)
+            if min(load) >= TEAM_MIN_SHARE * total:
+                break
+        sinks = [i for i in rest if not (users[i] & rest)]
+        if not sinks:
+            return None
+        i = max(sinks)
+        rest.discard(i)
+        join.add(i)
+        if sum(cost[j] for j in join) > TEAM_MAX_JOIN * total:
+            return None
+
+    def with_sources(members):
+        need = set(members)
+        stack = [j for i in members for j in deps[i] if dup[j]]
+        while stack:
+            j = stack.pop()
+            if j not in need:
+                need.add(j)
+                stack += [d for d in deps[j] if dup[d]]
+        return [ops[i] for i in sorted(need)]
+
+    side_of = {i: t for t in (0, 1) for i in sides[t]}
+    xfer: List[List[LV]] = [[], []]
+    seen: set = set()
+    for i in sorted(join):
+        for x in ops[i].ins:
+            r = x.root()
+            j = prod.get(id(r))
+            if j is None or j not in side_of or id(r) in seen:
+                continue
+            if planner.layout_of(r)[0] != ROW:
+                return None
+            seen.add(id(r))
+            xfer[side_of[j]].append(r)
+    return (with_sources(sides[0]), with_sources(sides[1]), with_sources(sorted(join)),
+            xfer[0], xfer[1])
 
 
 def _uniform_smem(rp: RowProgram) -> int:
@@ -597,6 +725,8 @@ class _Gen:
         self.rowed_names: Dict[int, List[str]] = {}
         self.uni_names: Dict[int, List[str]] = {}
         self.rng_ops: List[Tuple[LOp, int]] = []   # (op, count)
+        self.rng_slot: Dict[int, int] = {}          # id(op) -> index in rng_ops
+        self.scope_rows: set = set()  # rowed inputs declared in the current C++ scope
         self.outs: List[LV] = []
         self.tmp = 0
         # staged weights of rowed matvecs get a padded [K, Np] shared layout
@@ -677,6 +807,10 @@ class _Gen:
             return  # specialised immutable capture: read as literals (uni_elem)
         if id(r) in self.ptr_of:
             k = self.ptr_of[id(r)]
+            if (self.P.layout_of(x)[0] == ROW and id(r) in self.rowed_names
+                    and id(r) not in self.scope_rows):
+                self._declare_row_input(r, k, self.P.layout_of(x)[1])  # a new team scope
+                return
             if (self.P.layout_of(x)[0] == UNI and not self.rp.uniform_only
                     and id(r) not in self.uni_names):
                 # slot taken by a loop's stacked operand; stage it on its own too
@@ -690,18 +824,8 @@ class _Gen:
         L = self.P.layout_of(x)
         ct = _CTYPE[r.dtype]
         if L[0] == ROW:
-            w = L[1]
             self.ext_kind.append(ROW)
-            per_rep = []
-            for rep in range(self.R):
-                names = [f"i{k}_{j}{self.sfx(rep)}" for j in range(w)]
-                per_rep.append(names)
-                rv = self.rowv[rep]
-                self.body.append("    " + " ".join(
-                    f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{rv} * {w} + {j}];" if w > 1 else
-                    f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{rv}];"
-                    for j, nm in enumerate(names)))
-            self.rowed_names[id(r)] = per_rep
+            self._declare_row_input(r, k, L[1])
         elif self.rp.uniform_only:
             # uniform kernel: every global operand is put in flight at kernel
             # start (cp.async into shared memory), so the op loops that follow
@@ -721,6 +845,20 @@ class _Gen:
             pidx, _ = self._stage(r, f"s{k}", [k])
             self.uni_names[id(r)] = [self._lds(f"s{k}", p, False) for p in pidx]
             self.smem_name[id(r)] = (f"s{k}", False)
+
+    def _declare_row_input(self, r: LV, k: int, w: int) -> None:
+        ct = _CTYPE[r.dtype]
+        per_rep = []
+        for rep in range(self.R):
+            names = [f"i{k}_{j}{self.sfx(rep)}" for j in range(w)]
+            per_rep.append(names)
+            rv = self.rowv[rep]
+            self.body.append("    " + " ".join(
+                f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{rv} * {w} + {j}];" if w > 1 else
+                f"const {ct} {nm} = ((const {ct}*)a.p[{k}])[{rv}];"
+                for j, nm in enumerate(names)))
+        self.rowed_names[id(r)] = per_rep
+        self.scope_rows.add(id(r))
 
     def _stage(self, r: LV, name: str, slots: List[int]):
         """Stage uniform operand(s) of r's shape into shared array ``name``
@@ -994,8 +1132,8 @@ class _Gen:
         return self.uni_elem(x, j)
 
     # -- emission ---------------------------------------------------------------------
-    def emit(self) -> None:
-        for op in self.rp.ops:
+    def _emit_ops(self, ops) -> None:
+        for op in ops:
             if op.kind == "loop":
                 self._emit_loop(op)
                 continue
@@ -1008,6 +1146,55 @@ class _Gen:
                 self._emit_uniform_loop(op)
             else:
                 self._emit_rowed(op, L)
+
+    def _emit_teams(self) -> None:
+        """Team 0 / team 1 bodies and the join body (see find_teams): team 0
+        hands its values to the join in registers (tk*), team 1 through
+        shared memory (xf*, one slot per chain of the CTA)."""
+        t0, t1, join, x0, x1 = self.rp.teams
+        # Philox counter ranges are reserved in program order (as the eager
+        # draws consume them), not in the teams' emission order
+        for op in self.rp.ops:
+            for b in (op.body if op.kind == "loop" else (op,)):
+                if b.kind == "rng" and id(b) not in self.rng_slot:
+                    self.rng_ops.append((b, b.outs[0].numel))
+                    self.rng_slot[id(b)] = len(self.rng_ops) - 1
+        self.team_decls: List[str] = []
+        bodies = []
+        for t, (ops, xfer) in enumerate(((t0, x0), (t1, x1))):
+            self.body, self.scope_rows = [], set()
+            self._emit_ops(ops)
+            for lv in xfer:
+                ct = _CTYPE[lv.dtype]
+                for j, nm in enumerate(self.rowed_names[id(lv)][0]):
+                    if t == 0:
+                        self.team_decls.append(f"  {ct} tk{lv.id}_{j};")
+                        self.body.append(f"    tk{lv.id}_{j} = {nm};")
+                    else:
+                        self.team_decls.append(f"  __shared__ {ct} xf{lv.id}_{j}[64];")
+                        self.body.append(f"    xf{lv.id}_{j}[lid] = {nm};")
+            bodies.append(self.body)
+        self.body, self.scope_rows = [], set()
+        for t, xfer in enumerate((x0, x1)):
+            for lv in xfer:
+                ct = _CTYPE[lv.dtype]
+                names = []
+                for j in range(len(self.rowed_names[id(lv)][0])):
+                    nm = f"j{lv.id}_{j}"
+                    src = f"tk{lv.id}_{j}" if t == 0 else f"xf{lv.id}_{j}[lid]"
+                    self.body.append(f"    const {ct} {nm} = {src};")
+                    names.append(nm)
+                self.rowed_names[id(lv)] = [names]
+        self._emit_ops(join)
+        self.team_bodies = (bodies[0], bodies[1], self.body)
+        self.body = []
+
+    def emit(self) -> None:
+        if self.rp.teams is not None and not self.rp.uniform_only and self.R == 1:
+            self._emit_teams()
+        else:
+            self.rp.teams = None
+            self._emit_ops(self.rp.ops)
         if self.rp.uniform_only:
             self._uniform_prologue()
         for op in self.rp.ops:
@@ -1307,8 +1494,10 @@ class _Gen:
                 else:
                     lines.append(f"const {ct} {nm} = {red};")
         elif k == "rng":
-            self.rng_ops.append((op, o.numel))
-            slot = len(self.rng_ops) - 1
+            slot = self.rng_slot.get(id(op))
+            if slot is None:  # (a draw recomputed by two teams uses the same counters)
+                self.rng_ops.append((op, o.numel))
+                slot = self.rng_slot[id(op)] = len(self.rng_ops) - 1
             for rep in range(self.R):
                 rv = self.rowv[rep]
                 for j in range(w):
@@ -1360,15 +1549,23 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
             src_arr = g.uni_names[id(o)][0].split("[")[0]
             uni_stores.append(f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
                               f"(({ct}*)a.p[{k0 + t}])[q] = {src_arr}[q];")
+    if rp.teams is not None:
+        bodies = []
+        for body in g.team_bodies:
+            for t, o in enumerate(g.outs):
+                body = [b.replace(f"@O{o.id}@", str(k0 + t)) for b in body]
+            bodies.append(body)
+        g.team_bodies = bodies
     n_ptr = k0 + len(g.outs)
     n_rng = max(1, len(g.rng_ops))
     rp.block = g.block if rp.uniform_only else 128
+    rp.rows_per_cta = 64 if rp.teams is not None else 128 * rp.replicas
     mb = MIN_BLOCKS
     if not rp.uniform_only and mb == 0:
         # fit the whole batch in ONE wave when a register cap allows it: with
         # 1e5 chains, 782 CTAs need 6 per SM, i.e. <= 80 registers (an 87-
         # register kernel ran 5/SM and spilled 42 CTAs into a second wave)
-        per_sm = -(-(-(-rp.batch // (128 * rp.replicas))) // SM_COUNT)
+        per_sm = -(-(-(-rp.batch // rp.rows_per_cta)) // SM_COUNT)
         if 2 <= per_sm <= 7:
             mb = per_sm
     bounds = str(rp.block) if rp.uniform_only or mb == 0 else f"128, {mb}"
@@ -1396,6 +1593,23 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         src.append("}\n")
         core = "\n".join(src)
         name = "sf_uni_" + hashlib.sha1(core.encode()).hexdigest()[:16]
+        source = '#include "sf_ops.cuh"\n' + core.replace("KNAME", name)
+        return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr
+    if rp.teams is not None:
+        # two teams of two warps over the CTA's 64 chains (find_teams)
+        src.append("  const int team = threadIdx.x >> 6, lid = threadIdx.x & 63;")
+        src.append("  const long long r = (long long)blockIdx.x * 64 + lid;")
+        src.append("  const bool live = r < a.rows;")
+        src += g.team_decls
+        src.append("  if (live && team == 0) {")
+        src += g.team_bodies[0]
+        src.append("  }\n  if (live && team == 1) {")
+        src += g.team_bodies[1]
+        src.append("  }\n  __syncthreads();\n  if (live && team == 0) {")
+        src += g.team_bodies[2]
+        src.append("  }\n}\n")
+        core = "\n".join(src)
+        name = "sf_rows_" + hashlib.sha1(core.encode()).hexdigest()[:16]
         source = '#include "sf_ops.cuh"\n' + core.replace("KNAME", name)
         return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr
     # R chains per thread (rows r + 128 k of the CTA's 128 R rows; a replica

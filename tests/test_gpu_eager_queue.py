@@ -288,3 +288,79 @@ def test_identity_is_fresh_handle_and_reshape_is_view():
     z = sf.reshape(x, (2, 3))
     assert z.shape == (2, 3)
     np.testing.assert_array_equal(z.numpy(), np.arange(6, dtype=np.float32).reshape(2, 3))
+
+
+# -- the native staged-call path (StagedFast, csrc/sf_eager.cpp) ----------------
+
+
+def _staged_program():
+    rng = np.random.default_rng(5)
+    w = sf.constant(rng.standard_normal((4, 4)).astype(np.float32))
+    b = sf.constant(rng.standard_normal((1, 4)).astype(np.float32))
+
+    def body(x, y):
+        h = plugins.tanh(sf.add(sf.matmul(x, w), b))
+        return sf.mul(h, y), sf.reduce_sum(h)
+
+    return body
+
+
+def test_staged_fast_path_bitwise_and_counters():
+    plugins.install()
+    rng = np.random.default_rng(0)
+    xs = [sf.constant(rng.standard_normal((64, 4)).astype(np.float32)) for _ in range(4)]
+    y = sf.constant(np.full((64, 4), 0.5, np.float32))
+    results, snaps = {}, {}
+    for mode in ("queue", "python"):
+        rt = sf.init_runtime(sf.RuntimeOptions())
+        plugins.install()
+        with _Mode(mode):
+            f = sf.stage(_staged_program())
+            outs = [f(x, y) for x in xs]
+            results[mode] = [(a.numpy(), s.numpy()) for a, s in outs]
+            snaps[mode] = (rt.stats.snapshot(), f.cache_size)
+            if mode == "queue":
+                assert f._fast is not None  # armed after the first call
+    for (a0, s0), (a1, s1) in zip(results["queue"], results["python"]):
+        assert a0.tobytes() == a1.tobytes() and s0.tobytes() == s1.tobytes()
+    assert snaps["queue"] == snaps["python"]
+    assert snaps["queue"][0]["eager_op_counts"]["call_function"] == 4
+    assert snaps["queue"][0]["traces"] == 1
+
+
+def test_staged_fast_path_misses_fall_back():
+    plugins.install()
+    rt = sf.get_runtime()
+    f = sf.stage(_staged_program())
+    y = sf.constant(np.ones((8, 4), np.float32))
+    a = f(sf.constant(np.ones((8, 4), np.float32)), y)
+    launches = rt.stats.graph_launches
+    b = f(sf.constant(np.ones((8, 4), np.float32)), y)          # fast path
+    assert rt.stats.graph_launches == launches + 1
+    assert a[0].numpy().tobytes() == b[0].numpy().tobytes()
+    c = f(sf.constant(np.ones((16, 4), np.float32)),               # new shape: retrace
+          sf.constant(np.ones((16, 4), np.float32)))
+    assert c[0].shape == (16, 4) and f.cache_size == 2
+    with sf.Tape() as t:                                           # a tape: reference path
+        x = sf.constant(np.ones((8, 4), np.float32))
+        t.watch(x)
+        out, s = f(x, y)
+    g = t.gradient(s, x)
+    assert g.shape == (8, 4)
+    sf.init_runtime(sf.RuntimeOptions())                           # a new runtime: miss
+    plugins.install()
+    d = f(sf.constant(np.ones((8, 4), np.float32)), sf.constant(np.ones((8, 4), np.float32)))
+    assert d[0].numpy().tobytes() == a[0].numpy().tobytes()
+
+
+def test_l2hmc_staged_fast_path_matches_reference_path():
+    from paper_1903_01855_b200.workloads import l2hmc
+
+    outs = {}
+    for mode in ("queue", "python"):
+        sf.init_runtime(sf.RuntimeOptions(seed=3))
+        plugins.install()
+        with _Mode(mode):
+            s = l2hmc.L2HMCSampler(sf, 200, "staged", seed=0)
+            outs[mode] = np.stack([s.run_iteration() for _ in range(4)])
+    assert outs["queue"].tobytes() == outs["python"].tobytes()
