@@ -545,7 +545,7 @@ def plan_rows(ops: List[LOp], keep=frozenset()) -> List:
                 body = RowProgram(u.batch)
                 body.ops = reroll(row_ops, planner, users, keep) if REROLL else row_ops
                 chunks = _split(body, planner)
-                if 0 < batch <= TEAM_MAX_BATCH:
+                if 0 < batch <= team_max_batch():
                     for c in chunks:
                         if c.replicas == 1:
                             c.teams = find_teams(c, planner)
@@ -572,9 +572,15 @@ def plan_rows(ops: List[LOp], keep=frozenset()) -> List:
 # one part; the values the join needs cross through shared memory after one
 # barrier.  One thread's serial latency per chain halves, which is what
 # bounds small batches (C1: 200 chains, ~60 us of dependent instructions).
-# Above TEAM_MAX_BATCH chains the GPU is full with one chain per thread and
-# the split would only add a second wave.
-TEAM_MAX_BATCH = int(__import__("os").environ.get("SF_TEAM_MAX_BATCH", "40000"))
+# Only while the team-split grid (64 chains per CTA) stays within one CTA per
+# SM: measured on B200 (L2HMC, device time per transition), 10 - 2000 chains
+# 47 -> 35 us, but 1e4 chains (157 CTAs > 148 SMs) 46 -> 53 us.
+# SF_TEAM_MAX_BATCH overrides (0 disables).
+_TEAM_ENV = __import__("os").environ.get("SF_TEAM_MAX_BATCH")
+
+
+def team_max_batch() -> int:
+    return int(_TEAM_ENV) if _TEAM_ENV is not None else 64 * SM_COUNT
 TEAM_MIN_SHARE = 0.25   # each team carries at least this share of the work
 TEAM_MAX_JOIN = 0.10    # at most this share of the work runs after the barrier
 DUP_MAX_COST = 32       # ops computed from inputs alone up to this cost are recomputed per team
