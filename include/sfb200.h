@@ -176,6 +176,27 @@ int sf_rng(int dev, int kind, int dtype, int64_t n, uint64_t offset, void** out)
 int sf_dropout(int dev, int dtype, int64_t n, const void* x, const void* u, int u_dtype,
                double rate, void** out, void** mask);
 
+/* ------------------------------------------------------------ collectives
+ * NCCL (libnccl.so.2, opened at first use) for the data-parallel gradient
+ * all-reduce of config C5 — the build's only exchange step.  Each
+ * communicator owns a comm stream; an all-reduce is forked from the
+ * device's stream after the work enqueued so far and runs grouped and in
+ * place.  Staged plans issue them per gradient bucket as the backward
+ * produces the bucket (plan step 12) and join once at the end, so the
+ * transfers overlap the remaining backward kernels.
+ * Replaces: nothing in the reference (it has no distribution);
+ * SURVEY.md §8(b) sf_nccl_init / sf_allreduce. */
+/* 128-byte NCCL unique id (rank 0 creates it; every rank passes it to init) */
+int sf_comm_unique_id(void* id_out);
+int sf_comm_init(int dev, int nranks, int rank, const void* id, void** comm);
+int sf_comm_destroy(void* comm);
+/* Sum-all-reduce n buffers in place (counts in elements); scale != 1 sums
+ * scale * x (NCCL premul sum).  Ordered after earlier work on the device's
+ * stream; later work on it waits for the result. */
+int sf_allreduce(void* comm, void* const* bufs, const size_t* counts, int n, int dtype,
+                 double scale);
+int sf_nccl_version(int* version);
+
 /* ------------------------------------------------------- NN plugin kernels
  * (ResNet-50, configs C4/C5; no reference counterpart — the reference has no
  * convolution/pooling/xent).  NHWC; g8 = {N, H, W, C, KH, KW,

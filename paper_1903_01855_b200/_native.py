@@ -117,6 +117,14 @@ def _declare(lib: ctypes.CDLL) -> None:
                                                ctypes.POINTER(ctypes.c_double),
                                                ctypes.POINTER(ctypes.c_uint64)]),
         "sf_launch_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
+        "sf_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+        "sf_comm_init": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_char_p, _PVP]),
+        "sf_comm_destroy": (ctypes.c_int, [_VP]),
+        "sf_allreduce": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_void_p),
+                                         ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_double]),
+        "sf_nccl_version": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
         "sf_queue_push": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _PVP]),
         "sf_queue_flush": (ctypes.c_int, [ctypes.c_int]),
         "sf_queue_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64]),
@@ -155,6 +163,7 @@ EXPORTED_SYMBOLS = (
     "sf_while_buffer",
     "sf_while_capture_begin", "sf_while_set_cond", "sf_while_capture_end", "sf_while_launch",
     "sf_while_destroy", "sf_queue_push", "sf_queue_flush", "sf_queue_config", "sf_queue_stats",
+    "sf_comm_unique_id", "sf_comm_init", "sf_comm_destroy", "sf_allreduce", "sf_nccl_version",
 )
 
 
@@ -576,6 +585,46 @@ def launch_count(dev: int) -> int:
     c = ctypes.c_uint64(0)
     L.sf_launch_count(dev, ctypes.byref(c))
     return c.value
+
+
+def comm_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0 of a communicator creates it)."""
+    buf = ctypes.create_string_buffer(128)
+    rc = require_device().sf_comm_unique_id(buf)
+    if rc:
+        raise _err(_lib, rc, "sf_comm_unique_id")
+    return buf.raw
+
+
+def comm_init(dev: int, nranks: int, rank: int, uid: bytes) -> int:
+    h = ctypes.c_void_p(0)
+    rc = require_device().sf_comm_init(dev, nranks, rank, uid, ctypes.byref(h))
+    if rc:
+        raise _err(_lib, rc, "sf_comm_init")
+    return h.value
+
+
+def comm_destroy(handle: int) -> None:
+    if handle and _lib is not None:
+        _lib.sf_comm_destroy(handle)
+
+
+def allreduce(handle: int, ptrs: Sequence[int], counts: Sequence[int], dtype_tag: int,
+              scale: float = 1.0) -> None:
+    n = len(ptrs)
+    parr = (ctypes.c_void_p * max(1, n))(*ptrs)
+    carr = (ctypes.c_size_t * max(1, n))(*counts)
+    rc = lib().sf_allreduce(handle, parr, carr, n, dtype_tag, scale)
+    if rc:
+        raise _err(_lib, rc, "sf_allreduce")
+
+
+def nccl_version() -> int:
+    v = ctypes.c_int(0)
+    rc = require_device().sf_nccl_version(ctypes.byref(v))
+    if rc:
+        raise _err(_lib, rc, "sf_nccl_version")
+    return v.value
 
 
 def queue_flush(dev: int) -> None:

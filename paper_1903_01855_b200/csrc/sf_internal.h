@@ -190,6 +190,13 @@ struct RedGeom {
 };
 void reduce_geometry(int ndim, const int64_t* shape, uint32_t axes_mask, RedGeom* g);
 
+// NCCL (sf_comm.cpp): grouped in-place all-reduce forked from the device
+// stream onto the communicator's stream; comm_join makes the device stream
+// wait for everything enqueued so far
+int comm_allreduce(void* comm, Device* d, void* const* bufs, const size_t* counts, int n,
+                   int dtype, double scale);
+int comm_join(void* comm, Device* d);
+
 // Row-kernel constant pool (sf_plan.cpp step kind 1 with a pool section):
 // gather the kernel's uniform operands into `image` at their pool offsets
 // (rows of N elements padded to Np), then the image is copied into the

@@ -35,6 +35,9 @@
 //     kind 9 RNG       i32 kind | i32 dtype | i32 out | i32 pad | i64 n
 //     kind 10 DROPOUT  i32 dtype | i32 x | i32 out | i32 mask | i64 n | f64 rate
 //     kind 11 CAST     i32 src | i32 dst | i32 in | i32 out | i64 n
+//     kind 12 ALLREDUCE u64 comm | i32 dtype | i32 n | f64 scale | i32 slot[n]
+//                      (in place, on the communicator's stream, forked after the
+//                      steps so far; the plan joins it back after its last step)
 #include "sf_internal.h"
 
 namespace sfrt {
@@ -123,10 +126,29 @@ static int bad(const char* what) {
   return SF_ERR_INVALID;
 }
 
-static int run_step(Plan* p, Device* d, Step& s, std::vector<void*>& ptr) {
+static int run_step(Plan* p, Device* d, Step& s, std::vector<void*>& ptr,
+                    std::vector<void*>* comms) {
   const auto& b = s.payload;
   auto P = [&](int32_t slot) -> void* { return slot < 0 ? nullptr : ptr[slot]; };
   switch (s.kind) {
+    case 12: {
+      void* comm = (void*)at<uint64_t>(b, 0);
+      const int32_t dtype = at<int32_t>(b, 8), n = at<int32_t>(b, 12);
+      const double scale = at<double>(b, 16);
+      std::vector<void*> bufs(n);
+      std::vector<size_t> counts(n);
+      const size_t w = dtype_size(dtype);
+      for (int i = 0; i < n; ++i) {
+        const int32_t slot = at<int32_t>(b, 24 + 4 * i);
+        bufs[i] = P(slot);
+        counts[i] = p->slots[slot].nbytes / w;
+      }
+      SF_TRY(comm_allreduce(comm, d, bufs.data(), counts.data(), n, dtype, scale));
+      for (void* c : *comms)
+        if (c == comm) return SF_OK;
+      comms->push_back(comm);
+      return SF_OK;
+    }
     case 1: {  // JIT
       std::vector<char> blob(s.ptr_slots.size() * 8 + s.scalars.size());
       for (size_t i = 0; i < s.ptr_slots.size(); ++i) {
@@ -361,6 +383,7 @@ int sf_plan_run(void* plan, const void* const* inputs, void** outputs) {
   }
   int st = SF_OK;
   size_t k = 0;
+  std::vector<void*> comms;  // communicators with an all-reduce in flight
   for (; k < p->steps.size(); ++k) {
     Step& s = p->steps[k];
     for (int32_t slot : s.defs) {
@@ -369,13 +392,17 @@ int sf_plan_run(void* plan, const void* const* inputs, void** outputs) {
     }
     if (st != SF_OK) break;
     if (p->profile) cudaEventRecord(p->ev[2 * k], d->stream);
-    st = run_step(p, d, s, ptr);
+    st = run_step(p, d, s, ptr, &comms);
     if (st != SF_OK) break;
     if (p->profile) cudaEventRecord(p->ev[2 * k + 1], d->stream);
     for (int32_t slot : s.frees) {
       d->alloc.release(ptr[slot]);
       ptr[slot] = nullptr;
     }
+  }
+  for (void* c : comms) {  // the outputs are complete only after the collectives
+    const int js = comm_join(c, d);
+    if (st == SF_OK) st = js;
   }
   if (st != SF_OK) {
     // release everything this run allocated

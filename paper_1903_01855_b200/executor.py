@@ -15,7 +15,9 @@ copy accounting (:231-261), so copy counters stay identical.
 from __future__ import annotations
 
 import struct
+import threading
 import weakref
+from contextlib import contextmanager
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from . import _native, dtypes
@@ -119,8 +121,13 @@ class Program:
     """A graph function lowered for one device and input signature."""
 
     def __init__(self, gf: GraphFunction, inputs: Sequence, device, libraries, rng_mode: str,
-                 fuse_enabled: bool):
+                 fuse_enabled: bool, collective=None):
         self.gf = gf
+        # data-parallel gradient exchange (comm.py): (GradientCollective,
+        # output indices to sum over ranks) or None; the indices not reduced
+        # inside a plan are reduced after the run (post_reduce)
+        self.collective = collective
+        self.post_reduce: List[int] = []
         self.device = device
         self.dev = ordinal_of(device)
         self.keep: List = []  # constant tensors whose buffers plans point at
@@ -149,6 +156,9 @@ class Program:
         self.segments = self._segment(units)
         self.n_launches = sum(s.n_launches for s in self.segments
                               if isinstance(s, _NativeSegment))
+        if self.collective is not None:
+            self.post_reduce = [i for i in self.collective[1]
+                                if id(self.out_vals[i].root()) not in self._coll_done]
 
     # -- construction -------------------------------------------------------------
     def _segment(self, units) -> list:
@@ -159,8 +169,15 @@ class Program:
             for op in _unit_ops(unit):
                 for x in op.ins:
                     last_use[id(x.root())] = max(last_use.get(id(x.root()), -1), u)
+        self._read_by = dict(last_use)  # last unit reading each root (outputs aside)
         for v in self.out_vals:
             last_use[id(v.root())] = end
+        # collective outputs: root id -> index into out_vals (first occurrence)
+        self._coll_roots: Dict[int, int] = {}
+        if self.collective is not None:
+            for i in self.collective[1]:
+                self._coll_roots.setdefault(id(self.out_vals[i].root()), i)
+        self._coll_done: set = set()
         produced_in: Dict[int, int] = {}
         for u, unit in enumerate(units):
             for op in _unit_ops(unit):
@@ -248,6 +265,45 @@ class Program:
             return s
 
         n_launch = 0
+        coll = self.collective
+        pending: List[Tuple[int, int]] = []  # (slot, nbytes) awaiting their bucket
+        pending_bytes = 0
+        reduced_here: set = set()
+
+        def flush_bucket():
+            nonlocal pending, pending_bytes, n_launch
+            if not pending:
+                return
+            spec = coll[0]
+            slots = [sl for sl, _ in pending]
+            dtype = pw.slots[slots[0]][1]
+            payload = struct.pack("<Qiid", spec.comm.handle, dtype, len(slots), float(spec.scale))
+            payload += struct.pack("<%di" % len(slots), *slots)
+            pw.step(12, payload, uses=slots)
+            n_launch += 1
+            pending, pending_bytes = [], 0
+
+        def collect(u: int):
+            """Gradient outputs defined by now and read by nothing later join
+            the current bucket (in the order the backward produced them)."""
+            nonlocal pending_bytes
+            for rid, i in self._coll_roots.items():
+                if rid in reduced_here or rid in self._coll_done:
+                    continue
+                sl = slot_of.get(rid)
+                if sl is None or pw.slots[sl][0] != SLOT_OUTPUT or pw.slots[sl][5] < 0:
+                    continue
+                if self._read_by.get(rid, -1) > u:
+                    continue
+                if pending and pw.slots[pending[0][0]][1] != pw.slots[sl][1]:
+                    flush_bucket()  # one dtype per grouped call
+                reduced_here.add(rid)
+                nb = pw.slots[sl][3]
+                pending.append((sl, nb))
+                pending_bytes += nb
+                if pending_bytes >= coll[0].bucket_bytes:
+                    flush_bucket()
+
         for u_off, unit in enumerate(units):
             u = start + u_off
             if isinstance(unit, tuple):
@@ -271,6 +327,11 @@ class Program:
                                              group_def if inplace else slot_for_def)
             else:
                 n_launch += self._emit_op(pw, unit, slot_for_use, slot_for_def)
+            if coll is not None and self._coll_roots:
+                collect(u)
+        if coll is not None:
+            flush_bucket()
+            self._coll_done |= reduced_here
         pw.n_inputs = len(in_roots)
         pw.n_outputs = len(out_roots)
         seg = _NativeSegment()
@@ -472,6 +533,18 @@ class Program:
 
     # -- execution -----------------------------------------------------------------
     def run(self, inputs: Sequence, libraries) -> List[Tensor]:
+        outs = self._run(inputs, libraries)
+        if self.post_reduce:
+            # gradients no plan reduced (computed by Python segments, or
+            # aliases of inputs/constants): reduce copies after the run
+            spec = self.collective[0]
+            red = spec.comm.allreduce([outs[i] for i in self.post_reduce], spec.scale)
+            outs = list(outs)
+            for i, t in zip(self.post_reduce, red):
+                outs[i] = t
+        return outs
+
+    def _run(self, inputs: Sequence, libraries) -> List[Tensor]:
         g = self.__dict__.get("_replay")
         if g is not None and g is not False:
             outs = g.try_run(inputs)
@@ -494,7 +567,8 @@ class Program:
     def _replayable(self) -> bool:
         r = self.__dict__.get("_replayable_flag")
         if r is None:
-            r = (not self.has_rng and self.n_launches >= GRAPH_MIN_LAUNCHES
+            r = (not self.has_rng and self.collective is None
+                 and self.n_launches >= GRAPH_MIN_LAUNCHES
                  and all(s.op.name in GRAPH_SAFE_OPS for s in self.segments
                          if isinstance(s, _PySegment)))
             self._replayable_flag = r
@@ -623,6 +697,28 @@ def bakeable(ph, v) -> bool:
             and v.dtype.is_float and 0 < v.size <= BAKE_MAX_NUMEL and v in STABLE_CAPTURES)
 
 
+_collective_local = threading.local()
+
+
+@contextmanager
+def reduce_outputs(spec, outputs: Sequence[int]):
+    """Run graph functions in this block with ``outputs`` summed over the
+    ranks of ``spec.comm`` (comm.GradientCollective): the staged backward of
+    a data-parallel step."""
+    from .comm import output_spec
+
+    prev = _collective_local.__dict__.get("spec")
+    _collective_local.spec = (spec, tuple(outputs), output_spec(spec, outputs))
+    try:
+        yield
+    finally:
+        _collective_local.spec = prev
+
+
+def _output_collective():
+    return _collective_local.__dict__.get("spec")
+
+
 def _signature(inputs: Sequence) -> Tuple:
     return tuple((type(v).__name__ == "Variable", v.dtype, v.shape) for v in inputs)
 
@@ -644,7 +740,10 @@ def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
     # registry: a program from an earlier runtime is never reused
     pkey = (device, rt.generation, opts.rng, opts.fuse)
     last = gf.__dict__.get("_last_prog")
-    if last is not None and last[0] == pkey and len(last[1]) == len(inputs):
+    if _collective_local.__dict__.get("spec") is not None:
+        last = None  # keyed by the collective too (below)
+    if (last is not None and last[0] == pkey and len(last[1]) == len(inputs)
+            and last[3].collective is None):
         refs, comps, prog = last[1], last[2], last[3]
         baked = prog.baked
         for i, v in enumerate(inputs):
@@ -655,14 +754,17 @@ def _program_for(gf: GraphFunction, inputs, device, libraries) -> Program:
             refs[i] = weakref.ref(v)
         else:
             return prog
-    key = (pkey, _signature(inputs), _bake_key(gf, inputs))
+    coll = _output_collective()
+    key = (pkey, _signature(inputs), _bake_key(gf, inputs),
+           None if coll is None else coll[2])
     prog = cache.get(key)
     if prog is not None and any(r() is not inputs[i] for i, r in prog.baked.items()):
         prog = None  # an id reused by a different tensor
     if prog is None:
         if any(k[0][1] != rt.generation for k in cache):
             cache.clear()  # programs of a replaced runtime
-        prog = Program(gf, inputs, device, libraries, opts.rng, opts.fuse)
+        prog = Program(gf, inputs, device, libraries, opts.rng, opts.fuse,
+                       None if coll is None else coll[:2])
         cache[key] = prog
     gf._last_prog = (pkey, [weakref.ref(v) for v in inputs], list(key[1]), prog)
     return prog
