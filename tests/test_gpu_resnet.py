@@ -152,39 +152,3 @@ def test_resnet50_initial_gradients_match_reference(mode, dtype, tag, tol):
         scale = max(1e-30, float(np.abs(want).max()))
         err = float(np.abs(grads[i].numpy().ravel()[:want.size] - want).max()) / scale
         assert err < tol, (i, err)
-
-
-def test_resnet_dp_world1_matches_local_step():
-    """C5 plumbing on one GPU: NCCL world_size 1 through torch_view + buckets
-    on the backend stream must leave the SGD step bitwise equal to the local one."""
-    import socket
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_1903_01855_b200 import dist as sfdist
-
-    sf.init_runtime(sf.RuntimeOptions())
-    nn.install()
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
-    try:
-        torch.cuda.set_device(0)
-        sfdist.run_on_backend_stream(0)
-        dp = sfdist.ResNetDataParallel(sf, batch_per_rank=2, rank=0, world=1, image=32,
-                                       width_div=8)
-        local = resnet.ResNetTrain(sf, batch=1, mode="staged", image=32, seed=0, width_div=8)
-        for _ in range(2):
-            l_dp = dp.step().numpy()
-            l_loc = local.step(dp.x, dp.labels).numpy()
-            assert l_dp.tobytes() == l_loc.tobytes()
-        for a, b in zip(dp.train.model.params, local.model.params):
-            assert a.numpy().tobytes() == b.numpy().tobytes()
-        # the reducer really ran: buckets hold the last gradients
-        assert len(dp.reducer.buckets) >= 1
-        assert float(dp.reducer.flat[0].abs().sum()) > 0
-    finally:
-        dist.destroy_process_group()
-        torch.cuda.set_stream(torch.cuda.default_stream(0))
