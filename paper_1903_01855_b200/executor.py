@@ -399,7 +399,7 @@ class Program:
         n_rng = max(1, len(rng_counts))
         scalars = struct.pack("<qQ", rows, 0) + b"\0" * (8 * n_rng)
         block = rp.block  # one chain per thread; uniform kernels: one warp per op of a level
-        payload = struct.pack("<QIIII", kernel, grid, block, 0, len(ptrs))
+        payload = struct.pack("<QIIII", kernel, grid, block, rp.dyn_smem, len(ptrs))
         payload += struct.pack("<%di" % len(ptrs), *ptrs)
         payload += struct.pack("<I", len(scalars)) + scalars
         patches = [(0, 8, 0)] + [(1, 16 + 8 * i, c) for i, c in enumerate(rng_counts)]

@@ -32,7 +32,11 @@ ROW_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "rng", "eye"))
 MAX_UNIFORM_NUMEL = 1024       # uniform values computed per thread
 MAX_MATVEC = 1024              # k*n of a row matmul
 MAX_SMEM_BYTES = 40 * 1024     # uniform inputs staged in shared memory
-UNIFORM_SMEM_BYTES = 46 * 1024  # uniform kernel: results + staged operands (static smem)
+UNIFORM_SMEM_BYTES = 46 * 1024  # uniform kernel: results (static smem)
+# uniform kernel: global operands staged once into dynamic shared memory (a
+# chain of small layers, like C2's 100 (16,16) weights = 109 KB, then reads
+# every operand at shared-memory latency instead of an L2 round trip per layer)
+UNIFORM_DYN_BYTES = 200 * 1024
 MIN_BATCH = 2
 
 
@@ -99,7 +103,7 @@ REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 class RowProgram:
     __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas", "cpool", "teams",
-                 "rows_per_cta")
+                 "rows_per_cta", "dyn_smem")
 
     def __init__(self, batch: int):
         self.ops: List[LOp] = []
@@ -116,6 +120,7 @@ class RowProgram:
         # the program for the same 64 chains (find_teams), or None
         self.teams = None
         self.rows_per_cta = 128  # chains per CTA (set by code generation)
+        self.dyn_smem = 0  # dynamic shared memory bytes of the kernel
 
 
 class LoopOp:
@@ -748,10 +753,12 @@ class _Gen:
         # uniform kernel: staged global operands, CSE table, aliased results
         self.staged: Dict[int, str] = {}
         self.uni_smem = _uniform_smem(rp) if rp.uniform_only else 0
+        self.dyn = 0  # dynamic shared memory of the uniform kernel (staged operands)
         self.cse: Dict[tuple, LV] = {}
         self.alias: Dict[int, LV] = {}
         self.level: Dict[int, int] = {}
-        self.uni_ops: List[Tuple[int, int, str]] = []  # (level, work, code)
+        self.uni_ops: List[Tuple[int, int, str, tuple]] = []  # (level, work, code, out shape)
+        self.uni_entry: Dict[int, int] = {}  # uniform op output id -> its uni_ops entry
         self.block = 128
         self.f2vars: set = set()  # names declared float2 (packed row pairs)
         self.cpool = CONST_POOL and not rp.uniform_only
@@ -839,13 +846,14 @@ class _Gen:
             self.ext_kind.append(UNI)
             n = r.numel
             width = r.dtype.width
-            if width in (4, 8) and self.uni_smem + n * width <= UNIFORM_SMEM_BYTES:
-                self.uni_smem += n * width
-                self.staged[id(r)] = f"g{k}"
+            off = -(-self.dyn // 16) * 16
+            if width in (4, 8) and off + n * width <= UNIFORM_DYN_BYTES:
+                self.dyn = off + n * width
+                self.staged[id(r)] = f"((const {ct}*)(dsm + {off}))"
                 self.smem.append(
-                    f"  __shared__ __align__(16) {ct} g{k}[{max(1, n)}];\n"
                     f"  for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
-                    f"sf::cp_async<{width}>(&g{k}[q], &((const {ct}*)a.p[{k}])[q]);")
+                    f"sf::cp_async<{width}>(dsm + {off} + {width} * q, "
+                    f"&((const {ct}*)a.p[{k}])[q]);")
         else:
             self.ext_kind.append(UNI)
             pidx, _ = self._stage(r, f"s{k}", [k])
@@ -1037,6 +1045,20 @@ class _Gen:
                 return
             self.cse[key] = o
         level = 1 + max((self.level.get(id(self._canon(x)), -1) for x in op.ins), default=-1)
+        # an elementwise op whose newest operand is element-aligned with one
+        # op of the previous level (same output shape, so the same lane
+        # computes both elements) joins that op's loop: no barrier, no extra
+        # level (a chain like C2's matmul -> add -> tanh is one level per
+        # layer instead of three)
+        fold = None
+        if op.kind == "ew" and level > 0:
+            top = [x for x in op.ins if self.level.get(id(self._canon(x)), -1) == level - 1]
+            srcs = {id(self._canon(x)) for x in top}
+            if len(srcs) == 1 and all(x.shape == o.shape for x in top):
+                e = self.uni_entry.get(next(iter(srcs)))
+                if e is not None and self.uni_ops[e][3] == o.shape:
+                    fold = e
+                    level -= 1
         self.level[id(o)] = level
         self.smem.append(f"  __shared__ __align__(16) {ct} U{o.id}[{max(1, n)}];")
         self.uni_names[id(o)] = [f"U{o.id}[{q}]" for q in range(n)]
@@ -1096,14 +1118,21 @@ class _Gen:
         work = n * (op.ins[0].shape[-1] if k == "matmul" else 1)
         if k == "reduce":
             work = op.ins[0].numel
-        self.uni_ops.append((level, work, loop + body + " }"))
+        if fold is not None:
+            lv, wk, code, shp = self.uni_ops[fold]
+            # same loop: insert the body before the loop's closing brace
+            self.uni_ops[fold] = (lv, wk + work, code[:-2] + " " + body + " }", shp)
+            self.uni_entry[id(o)] = fold
+            return
+        self.uni_entry[id(o)] = len(self.uni_ops)
+        self.uni_ops.append((level, work, loop + body + " }", shape))
 
     def _uniform_prologue(self) -> None:
         """Level-by-level schedule of the uniform ops over up to 32 warps."""
         if not self.uni_ops:
             return
         levels: Dict[int, List[Tuple[int, str]]] = {}
-        for level, work, code in self.uni_ops:
+        for level, work, code, _shape in self.uni_ops:
             levels.setdefault(level, []).append((work, code))
         warps = max(1, min(32, max(len(v) for v in levels.values())))
         self.block = 32 * warps
@@ -1597,6 +1626,9 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         src.append("  if (blockIdx.x == 0) {\n    " + "\n    ".join(uni_stores) + "\n  }")
     if rp.uniform_only:
         src.append("}\n")
+        rp.dyn_smem = g.dyn
+        if g.dyn:
+            src.insert(2, "  extern __shared__ __align__(16) unsigned char dsm[];")
         core = "\n".join(src)
         name = "sf_uni_" + hashlib.sha1(core.encode()).hexdigest()[:16]
         source = '#include "sf_ops.cuh"\n' + core.replace("KNAME", name)
