@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <memory>
 
+#include <atomic>
+
 #include "sf_internal.h"
 #include "sf_ops_embed.h"  // generated: const char* kSfOpsCuh
 
@@ -25,6 +27,7 @@ struct JitKernel {
   std::mutex pool_mu;  // constant-pool fill + launch are one unit per module
   CUmodule module[64] = {};
   CUfunction fn[64] = {};
+  std::atomic<unsigned> dyn_smem[64] = {};  // dynamic shared memory opted in per device
 };
 
 static std::mutex g_jit_mu;
@@ -182,8 +185,11 @@ int jit_launch(Device* d, void* kernel, unsigned grid, unsigned block, unsigned 
                const void* params, size_t params_bytes) {
   CUfunction f;
   SF_TRY(jit_function((JitKernel*)kernel, d->id, &f));
-  if (smem > 48 * 1024) {
+  // any dynamic shared memory is opted in (static + dynamic may pass 48 KB)
+  JitKernel* jk = (JitKernel*)kernel;
+  if (smem > jk->dyn_smem[d->id].load(std::memory_order_relaxed)) {
     SF_CHECK_CU(drv.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem));
+    jk->dyn_smem[d->id].store(smem, std::memory_order_relaxed);
   }
   size_t sz = params_bytes;
   void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params),

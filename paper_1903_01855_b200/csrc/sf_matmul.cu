@@ -122,11 +122,17 @@ __global__ void gemm_small(const T* __restrict__ A, const T* __restrict__ B, T* 
 template <class T, bool TA, bool TB>
 static void gemm_go(Device* d, const T* A, const T* B, T* C, long long m, long long n, long long k) {
   const long long tiles64 = ((n + 63) / 64) * ((m + 63) / 64);
-  // one thread per output also when the 64x64 tiling would leave most SMs
-  // idle (a classifier layer: m = batch, n = 1000, k = 2048 -> 16 tiles) and
-  // there are enough outputs to fill them; the k order is the same
-  const bool few_tiles = tiles64 * 2 < d->sm_count && m * n >= 8192 && k < 16384;
-  if ((m * n <= 4096 && k <= 256) || k <= 8 || few_tiles) {
+  // a 64x64 tiling that would leave most SMs idle (a classifier layer:
+  // m = batch, n = 1000, k = 2048 -> 16 tiles) splits k instead (below).
+  // One thread per output with a 2048-long dependent FMA chain was latency-
+  // bound: 358 us per launch in the ResNet-50 step (profiles/r02e).  Only
+  // long contractions split, so every matmul a fused kernel inlines
+  // (k * n <= 1024) keeps the sequential-k order; eager and staged run this
+  // same kernel, so they agree bit for bit either way.
+  // (float64 keeps the sequential-k order everywhere: the f64 parity runs
+  // compare whole training trajectories against the reference at 1e-9)
+  const bool few_tiles = sizeof(T) == 4 && tiles64 * 2 < d->sm_count && k >= 512;
+  if ((m * n <= 4096 && k <= 256) || k <= 8) {
     long long blocks = (m * n + 255) / 256;
     if (blocks > d->sm_count * 16LL) blocks = d->sm_count * 16LL;
     if (blocks < 1) blocks = 1;
@@ -134,12 +140,13 @@ static void gemm_go(Device* d, const T* A, const T* B, T* C, long long m, long l
   } else {
     const long long tiles = ((n + 63) / 64) * ((m + 63) / 64);
     long long splits = 1;
-    // Long contractions over few output tiles (conv weight gradients: k = N*H*W)
-    // are split along k.  Only k >= 16384 splits, so every matmul a fused
-    // staged kernel can inline (k*n <= 1024) keeps the sequential-k order.
-    if (k >= 16384 && tiles < 2LL * d->sm_count) {
+    // Long contractions over few output tiles (conv weight gradients: k = N*H*W;
+    // the classifier layer) are split along k.  Only k >= 16384, or k >= 512
+    // over few tiles, splits, so every matmul a fused staged kernel can
+    // inline (k*n <= 1024) keeps the sequential-k order.
+    if ((k >= 16384 || few_tiles) && tiles < 2LL * d->sm_count) {
       splits = (2LL * d->sm_count + tiles - 1) / tiles;
-      const long long by_k = k / 4096;
+      const long long by_k = k >= 16384 ? k / 4096 : k / 256;
       if (splits > by_k) splits = by_k;
       if (splits > 64) splits = 64;
       if (splits < 1) splits = 1;

@@ -847,7 +847,9 @@ class _Gen:
             n = r.numel
             width = r.dtype.width
             off = -(-self.dyn // 16) * 16
-            if width in (4, 8) and off + n * width <= UNIFORM_DYN_BYTES:
+            # static (result arrays) + dynamic shared memory <= 227 KB per CTA
+            budget = min(UNIFORM_DYN_BYTES, 224 * 1024 - self.uni_smem)
+            if width in (4, 8) and off + n * width <= budget:
                 self.dyn = off + n * width
                 self.staged[id(r)] = f"((const {ct}*)(dsm + {off}))"
                 self.smem.append(
