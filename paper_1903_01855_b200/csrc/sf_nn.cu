@@ -47,48 +47,69 @@ __device__ __forceinline__ void split4(const float4 v, float4& h, float4& l) {
   h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
 }
 
-// One warp per (output pixel m, tap t); tap t == KH*KW (when kp > K) zero-fills
-// the K..kp padding of row m.  SPLIT: out = TF32 hi part, lo = remainder.
-template <class T, bool SPLIT>
-__global__ void im2col_seg_kernel(const T* __restrict__ x, T* __restrict__ out,
-                                  float* __restrict__ lo, ConvGeom g, int kp) {
+// im2col, NHWC, 16-byte vectors: work items are (segment,
+// 16-byte vector) pairs flattened over the whole output, and each thread
+// keeps UNROLL items' loads in flight before it stores any of them (a
+// one-warp-per-segment form left half the warp idle at C = 64 — the
+// 3x3 convolutions of layer1 — and waited one HBM round trip per segment:
+// ~1.1 TB/s in the ResNet-50 step, profiles/r02e_resnet50_step.md).
+template <class T, bool SPLIT, int UNROLL>
+__global__ void __launch_bounds__(256) im2col_vec_kernel(const T* __restrict__ x,
+                                                         T* __restrict__ out,
+                                                         float* __restrict__ lo, ConvGeom g,
+                                                         int kp) {
   using V = typename Vec16<T>::type;
   constexpr int VW = Vec16<T>::n;
   const int C = (int)g.c, KW = (int)g.kw, KK = (int)(g.kh * g.kw), K = KK * C;
+  const int CV = C / VW, PV = (kp - K) / VW;  // vectors per tap, per K padding
+  const int SV = CV > PV ? CV : PV;           // item slots per (row, tap)
   const int taps = KK + (kp > K ? 1 : 0);
   const int WO = (int)g.wo, HO = (int)g.ho, W = (int)g.w, H = (int)g.h;
-  const int nseg = (int)(g.n * g.ho * g.wo) * taps;
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += nwarps) {
-    const int m = s / taps, t = s - m * taps;
-    T* dst = out + (long long)m * kp;
-    float* dlo = SPLIT ? lo + (long long)m * kp : nullptr;
-    if (t == KK) {  // K padding
-      for (int k = K + lane; k < kp; k += 32) {
-        dst[k] = T(0);
-        if (SPLIT) dlo[k] = 0.f;
+  const int S = (int)g.s, P = (int)g.p;
+  // 32-bit index math throughout (the host checks rows * kp < 2^31): 64-bit
+  // divisions made this copy ALU-bound
+  const unsigned total = (unsigned)(g.n * g.ho * g.wo) * (unsigned)(taps * SV);
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned base = blockIdx.x * blockDim.x + threadIdx.x; base < total;
+       base += stride * UNROLL) {
+    V v[UNROLL];
+    long long dst[UNROLL];  // element offset of the item in out (-1: none)
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const unsigned i = base + (unsigned)u * stride;
+      dst[u] = -1;
+      if (i >= total) continue;
+      const unsigned sgm = i / (unsigned)SV;
+      const int q = (int)(i - sgm * (unsigned)SV);
+      const int m = (int)(sgm / (unsigned)taps), t = (int)(sgm - (unsigned)m * (unsigned)taps);
+      if (t == KK) {  // K padding: zeros in the first PV vectors of the tap slot
+        if (q < PV) {
+          memset(&v[u], 0, sizeof(V));
+          dst[u] = (long long)m * kp + K + (long long)q * VW;
+        }
+        continue;
       }
-      continue;
+      if (q >= CV) continue;
+      const int kh = t / KW, kw = t - kh * KW;
+      const int t2 = (int)((unsigned)m / (unsigned)WO), ow = m - t2 * WO;
+      const int n = (int)((unsigned)t2 / (unsigned)HO), oh = t2 - n * HO;
+      const int ih = oh * S - P + kh, iw = ow * S - P + kw;
+      if (ih >= 0 && ih < H && iw >= 0 && iw < W)
+        v[u] = reinterpret_cast<const V*>(x + (unsigned)((n * H + ih) * W + iw) * (unsigned)C)[q];
+      else
+        memset(&v[u], 0, sizeof(V));
+      dst[u] = (long long)m * kp + (long long)t * C + (long long)q * VW;
     }
-    const int kh = t / KW, kw = t - kh * KW;
-    const int ow = m % WO, t2 = m / WO;
-    const int oh = t2 % HO, n = t2 / HO;
-    const int ih = oh * (int)g.s - (int)g.p + kh, iw = ow * (int)g.s - (int)g.p + kw;
-    const bool inside = ih >= 0 && ih < H && iw >= 0 && iw < W;
-    const V* src = reinterpret_cast<const V*>(x + ((long long)(n * H + ih) * W + iw) * C);
-    V* d = reinterpret_cast<V*>(dst + t * C);
-    for (int q = lane; q < C / VW; q += 32) {
-      V v;
-      if (inside) v = src[q];
-      else memset(&v, 0, sizeof(V));
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (dst[u] < 0) continue;
       if constexpr (SPLIT) {
         float4 h, l;
-        split4(v, h, l);
-        d[q] = h;
-        reinterpret_cast<float4*>(dlo + t * C)[q] = l;
+        split4(v[u], h, l);
+        *reinterpret_cast<float4*>(out + dst[u]) = h;
+        *reinterpret_cast<float4*>(lo + dst[u]) = l;
       } else {
-        d[q] = v;
+        *reinterpret_cast<V*>(out + dst[u]) = v[u];
       }
     }
   }
@@ -127,6 +148,57 @@ __global__ void col2im_vec_kernel(const T* __restrict__ dcols, T* __restrict__ d
         for (int j = 0; j < VW; ++j) acc[j] = any ? sf::add(acc[j], e[j]) : e[j];
         any = true;
       }
+    }
+    V out;
+    T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) o[j] = any ? acc[j] : T(0);
+    reinterpret_cast<V*>(dx + (long long)pix * C)[cv] = out;
+  }
+}
+
+// col2im for KH x KW <= 3 x 3 filters: the taps unrolled at compile time, so
+// every contributing tap's load is issued before the (in-order) adds — the
+// same sum as col2im_vec_kernel (taps kh, kw ascending), without its
+// one-dependent-load-per-tap scan (~2.5 TB/s in the ResNet-50 step)
+template <class T, int KH, int KW>
+__global__ void __launch_bounds__(256) col2im_small_kernel(const T* __restrict__ dcols,
+                                                           T* __restrict__ dx, ConvGeom g) {
+  using V = typename Vec16<T>::type;
+  constexpr int VW = Vec16<T>::n;
+  const int C = (int)g.c, CV = C / VW, K = KH * KW * C;
+  const int W = (int)g.w, H = (int)g.h, WO = (int)g.wo, HO = (int)g.ho;
+  const int S = (int)g.s, P = (int)g.p;
+  const int total = (int)(g.n * g.h * g.w) * CV;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int cv = i % CV, pix = i / CV;
+    const int w = pix % W, t2 = pix / W;
+    const int h = t2 % H, n = t2 / H;
+    V buf[KH * KW];
+    bool ok[KH * KW];
+#pragma unroll
+    for (int kh = 0; kh < KH; ++kh) {
+#pragma unroll
+      for (int kw = 0; kw < KW; ++kw) {
+        const int y = h + P - kh, xx = w + P - kw;
+        const int oh = y / S, ow = xx / S;
+        const bool v = y >= 0 && xx >= 0 && y - oh * S == 0 && xx - ow * S == 0 && oh < HO &&
+                       ow < WO;
+        ok[kh * KW + kw] = v;
+        if (v)
+          buf[kh * KW + kw] = reinterpret_cast<const V*>(
+              dcols + (long long)((n * HO + oh) * WO + ow) * K + (kh * KW + kw) * C)[cv];
+      }
+    }
+    T acc[VW];
+    bool any = false;
+#pragma unroll
+    for (int t = 0; t < KH * KW; ++t) {
+      if (!ok[t]) continue;
+      const T* e = reinterpret_cast<const T*>(&buf[t]);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) acc[j] = any ? sf::add(acc[j], e[j]) : e[j];
+      any = true;
     }
     V out;
     T* o = reinterpret_cast<T*>(&out);
@@ -560,8 +632,8 @@ int sf_im2col(int dev, int dtype, const int64_t* g8, const void* x, void** cols)
     using T = decltype(t);
     const long long K = g.kh * g.kw * g.c;
     if (seg_ok(g, K, 16 / (int)sizeof(T))) {
-      const long long segs = g.n * g.ho * g.wo * g.kh * g.kw;
-      im2col_seg_kernel<T, false><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
+      const long long items = g.n * g.ho * g.wo * g.kh * g.kw * (g.c / (16 / (long long)sizeof(T)));
+      im2col_vec_kernel<T, false, 4><<<grid_for_n(d, (items + 3) / 4), 256, 0, d->stream>>>(
           (const T*)x, (T*)*cols, nullptr, g, (int)K);
     } else {
       im2col_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)x, (T*)*cols, g);
@@ -583,12 +655,16 @@ int sf_im2col_split(int dev, const int64_t* g8, int64_t kp, const void* x, void*
   if (total == 0) return SF_OK;
   count_launch(dev);
   if (seg_ok(g, kp, 4)) {
-    const long long segs = g.n * g.ho * g.wo * (g.kh * g.kw + 1);
+    const long long K = g.kh * g.kw * g.c;
+    const long long taps = g.kh * g.kw + (kp > K ? 1 : 0);
+    const long long sv = g.c / 4 > (kp - K) / 4 ? g.c / 4 : (kp - K) / 4;
+    const long long items = g.n * g.ho * g.wo * taps * sv;
+    const unsigned grid = grid_for_n(d, (items + 3) / 4);
     if (lo)
-      im2col_seg_kernel<float, true><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
+      im2col_vec_kernel<float, true, 4><<<grid, 256, 0, d->stream>>>(
           (const float*)x, (float*)*hi, (float*)*lo, g, (int)kp);
     else
-      im2col_seg_kernel<float, false><<<grid_for_n(d, segs * 32), 256, 0, d->stream>>>(
+      im2col_vec_kernel<float, false, 4><<<grid, 256, 0, d->stream>>>(
           (const float*)x, (float*)*hi, nullptr, g, (int)kp);
   } else if (!lo && total < (1ll << 31) - (1ll << 24) && g.n * g.h * g.w * g.c < (1ll << 31)) {
     im2col_rows_kernel<<<grid_for_n(d, g.n * g.ho * g.wo * 32), 256, 0, d->stream>>>(
@@ -616,8 +692,13 @@ int sf_col2im(int dev, int dtype, const int64_t* g8, const void* dcols, void** d
     using T = decltype(t);
     constexpr int vw = 16 / (int)sizeof(T);
     if (seg_ok(g, g.kh * g.kw * g.c, vw)) {
-      col2im_vec_kernel<T><<<grid_for_n(d, total / vw), 256, 0, d->stream>>>(
-          (const T*)dcols, (T*)*dx, g);
+      const unsigned grid = grid_for_n(d, total / vw);
+      if (g.kh == 3 && g.kw == 3)
+        col2im_small_kernel<T, 3, 3><<<grid, 256, 0, d->stream>>>((const T*)dcols, (T*)*dx, g);
+      else if (g.kh == 1 && g.kw == 1)
+        col2im_small_kernel<T, 1, 1><<<grid, 256, 0, d->stream>>>((const T*)dcols, (T*)*dx, g);
+      else
+        col2im_vec_kernel<T><<<grid, 256, 0, d->stream>>>((const T*)dcols, (T*)*dx, g);
     } else {
       col2im_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)dcols, (T*)*dx, g);
     }
