@@ -738,34 +738,43 @@ def resnet_extra(sf, np, _native):
         del tr
     row["staged_over_eager"] = row["staged"]["img_per_sec"] / row["eager"]["img_per_sec"]
     # roofline of the dominant tensor kernel: the tcgen05 3xTF32 GEMM at the
-    # shape of layer1's 3x3 convolution (M = 32*56*56, N = 64, K = 576),
-    # timed back to back with CUDA events on the backend stream
+    # shape of layer1's 3x3 convolution (M = 32*56*56, N = 64, K = 576), in
+    # the variant the training step runs (raw fp32 operands, the tf32 lo
+    # parts derived in shared memory), timed back to back with CUDA events
     peaks, kind = _peaks()
+    cpk = _compute_peaks()
     m, n, k = 32 * 56 * 56, 64, 576
     a = sf.constant(np.random.default_rng(0).standard_normal((m, k)).astype(np.float32))
     b = sf.constant(np.random.default_rng(1).standard_normal((n, k)).astype(np.float32))
-    ahi, alo = _native.split_tf32(0, m, k, a._ptr())
-    bhi, blo = _native.split_tf32(0, n, k, b._ptr())
     stream = torch.cuda.ExternalStream(_native.stream_of(0))
+
+    def gemm():
+        return _native.gemm_tf32x3_ex(0, m, n, k, False, False, k, k, a._ptr(), 0, b._ptr(), 0)
+
     for _ in range(3):
-        _native.gemm_tf32x3(0, m, n, k, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr)
+        gemm()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 20
     e0.record(stream)
     for _ in range(reps):
-        _native.gemm_tf32x3(0, m, n, k, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr)
+        gemm()
     e1.record(stream)
     _native.sync(0)
     ms = e0.elapsed_time(e1) / reps
     useful = 2.0 * m * n * k / (ms * 1e-3) / 1e12
-    peak = peaks.get("bf16_tflops", 1590.0)
-    row["roofline"] = {"kernel": "gemm_tc_kernel (tcgen05 kind::tf32, 3 passes)",
+    tf32 = cpk.get("tcgen05_tf32_tflops")
+    peak = tf32 / 3 if tf32 else peaks.get("bf16_tflops", 1590.0) / 6
+    row["roofline"] = {"kernel": "gemm_tc_persistent (tcgen05 kind::tf32, 3 passes, lo parts "
+                                 "derived in shared memory)",
                        "shape_mnk": [m, n, k], "ms": ms, "bound": "tensor",
                        "achieved": useful, "unit": "TFLOP/s (useful fp32 MACs x2)",
                        "peak": peak, "frac": useful / peak,
                        "tensor_issue_tflops": 3 * useful,
-                       "peak_kind": f"{kind} bf16 dense (TF32 is half of it; 3xTF32 issues "
-                                    "3 MMAs per useful MAC)"}
+                       "peak_kind": ("measured tcgen05 kind::tf32 dense / 3 (3xTF32 issues 3 MMAs "
+                                     "per useful MAC; profiles/r02_peaks.json)" if tf32 else
+                                     f"{kind} bf16 dense / 6 (TF32 = half, 3 passes)"),
+                       "step_useful_tflops": row["staged"]["useful_tflops"],
+                       "step_frac": row["staged"]["useful_tflops"] / peak}
     return row
 
 

@@ -28,9 +28,12 @@ namespace sfrt {
 
 static constexpr int TC_BM = 128, TC_BK = 32, TC_STAGES = 3;
 // smem ring depth: 64 KB stages (BN = 128) fit 3, 48 KB stages (BN = 64) fit 4
+// (BN = 256: 96 KB stages, 2 fit; each 128x256x8 MMA reads 12 KB of shared
+// memory per 128 tensor cycles vs 8 KB per 64 at BN = 128 — 25% less operand
+// traffic per MAC on the pipe that bounds the 3xTF32 passes)
 template <int BN>
 struct TcStages {
-  static constexpr int n = BN <= 64 ? 4 : 3;
+  static constexpr int n = BN <= 64 ? 4 : (BN <= 128 ? 3 : 2);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -591,6 +594,14 @@ int launch_gemm_tc_ex(Device* d, int64_t M, int64_t N, int64_t K, bool amn, bool
     return SF_ERR_INVALID;
   }
   if (N <= 64) return run_tc_major<64>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
+  // 256-wide tiles where they still give every SM a tile
+  static const int bn256 = [] {
+    const char* e = getenv("SF_GEMM_BN256");
+    return e ? atoi(e) : 1;
+  }();
+  const long long tiles256 = ((N + 255) / 256) * ((M + TC_BM - 1) / TC_BM);
+  if (bn256 && N >= 256 && tiles256 >= d->sm_count)
+    return run_tc_major<256>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
   return run_tc_major<128>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
 }
 

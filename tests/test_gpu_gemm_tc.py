@@ -56,7 +56,8 @@ def test_split_transpose_padding():
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, True), (True, False), (True, True)])
 @pytest.mark.parametrize("m,n,k,ak,bk", [(128, 64, 64, 64, 64), (200, 96, 100, 100, 97),
-                                         (516, 256, 3000, 3000, 3000), (36, 128, 33, 33, 33)])
+                                         (516, 256, 3000, 3000, 3000), (36, 128, 33, 33, 33),
+                                         (9600, 512, 96, 96, 96)])  # 256-wide tiles
 def test_gemm_mn_major_operands(a_mn, b_mn, m, n, k, ak, bk):
     """MN-major operands (A stored k x m, B stored k x n) read straight by TMA,
     no transposed copies; an operand holding fewer than k contraction rows
@@ -91,7 +92,8 @@ def test_gemm_mn_major_operands(a_mn, b_mn, m, n, k, ak, bk):
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
 @pytest.mark.parametrize("lo_a,lo_b", [(True, True), (True, False), (False, True)])
 @pytest.mark.parametrize("m,n,k,ak,bk", [(128, 64, 64, 64, 64), (200, 96, 100, 100, 97),
-                                         (516, 256, 3000, 3000, 3000), (1000, 200, 36, 36, 33)])
+                                         (516, 256, 3000, 3000, 3000), (1000, 200, 36, 36, 33),
+                                         (9600, 512, 96, 96, 96)])  # 256-wide tiles
 def test_gemm_lo_in_shared_memory_bitwise(a_mn, b_mn, lo_a, lo_b, m, n, k, ak, bk):
     """A NULL lo pointer makes the GEMM derive that operand's tf32 lo part in
     shared memory from the raw fp32 tile (converter warps) instead of reading
