@@ -34,12 +34,23 @@ def _f32(sf, arr):
 
 
 class _Net:
-    """GenericNet: h = relu(relu(V v + X x + T t) H); three heads."""
+    """GenericNet: h = relu(relu(V v + X x + T t) H); three heads.
+    ``trainable``: the weights are Variables (L2HMCTrain) instead of
+    immutable tensors."""
 
-    def __init__(self, sf, rng, factor):
+    def __init__(self, sf, rng, factor, trainable: bool = False):
+        def param(arr):
+            t = _f32(sf, arr)
+            if trainable:
+                t = sf.Variable(t)
+                self.variables.append(t)
+            return t
+
+        self.variables = []
+
         def dense(n_in, n_out, f):
             w = rng.standard_normal((n_in, n_out)) * math.sqrt(2.0 * f / n_in)
-            return _f32(sf, w), _f32(sf, np.zeros((1, n_out)))
+            return param(w), param(np.zeros((1, n_out)))
 
         self.v = dense(X_DIM, N_HIDDEN, 1.0 / 3.0)
         self.x = dense(X_DIM, N_HIDDEN, factor / 3.0)
@@ -48,8 +59,8 @@ class _Net:
         self.scale = dense(N_HIDDEN, X_DIM, 0.001)
         self.transl = dense(N_HIDDEN, X_DIM, 0.001)
         self.transf = dense(N_HIDDEN, X_DIM, 0.001)
-        self.coeff_scale = _f32(sf, np.zeros((1, X_DIM)))
-        self.coeff_transf = _f32(sf, np.zeros((1, X_DIM)))
+        self.coeff_scale = param(np.zeros((1, X_DIM)))
+        self.coeff_transf = param(np.zeros((1, X_DIM)))
 
 
 class L2HMCSampler:
@@ -68,7 +79,7 @@ class L2HMCSampler:
     gate_tol = 1e-5
 
     def __init__(self, sf, batch: int, mode: str = "staged", seed: int = 0,
-                 draws: str = "runtime", draw_seed: int = 0):
+                 draws: str = "runtime", draw_seed: int = 0, trainable: bool = False):
         if draws not in ("runtime", "inputs"):
             raise ValueError(f"draws must be 'runtime' or 'inputs', got {draws!r}")
         self.sf = sf
@@ -76,8 +87,9 @@ class L2HMCSampler:
         self.draws = draws
         self.draw_rng = np.random.default_rng(draw_seed)
         rng = np.random.default_rng(seed)
-        self.position_fn = _Net(sf, rng, 2.0)
-        self.momentum_fn = _Net(sf, rng, 1.0)
+        self.position_fn = _Net(sf, rng, 2.0, trainable)
+        self.momentum_fn = _Net(sf, rng, 1.0, trainable)
+        self.variables = self.position_fn.variables + self.momentum_fn.variables
         self.sigma_inv = _f32(sf, np.linalg.inv(SIGMA))
         self.ts = [_f32(sf, [[math.cos(2 * math.pi * i / N_STEPS),
                               math.sin(2 * math.pi * i / N_STEPS)]]) for i in range(N_STEPS)]
@@ -202,6 +214,11 @@ class L2HMCSampler:
         return x_post, v_post, prob
 
     def apply_transition(self, x, v_fwd=None, v_bwd=None, u_dir=None, u_acc=None):
+        x_out, accept_prob, _x_post = self.propose(x, v_fwd, v_bwd, u_dir, u_acc)
+        return x_out, accept_prob
+
+    def propose(self, x, v_fwd=None, v_bwd=None, u_dir=None, u_acc=None):
+        """(state after the MH step, acceptance probability, the proposal)."""
         sf = self.sf
         b = self.batch
         x_f, _v_f, p_f = self.transition_kernel(x, True, v_fwd)
@@ -218,7 +235,7 @@ class L2HMCSampler:
         acc = self._op("cast", sf.greater(accept_prob, u_acc), dtype=sf.float32)
         acc2 = sf.reshape(acc, (b, 1))
         x_out = sf.add(sf.mul(acc2, x_post), sf.mul(sf.reshape(sf.sub(1.0, acc), (b, 1)), x))
-        return x_out, accept_prob
+        return x_out, accept_prob, x_post
 
     # -- harness -------------------------------------------------------------------
     def host_draws(self):
@@ -247,3 +264,70 @@ class L2HMCSampler:
 
     def cache_size(self) -> int:
         return sum(pf.cache_size for pf in self.staged_functions)
+
+
+class L2HMCTrain:
+    """Training the L2HMC sampler (the paper's L2HMC figure: PAPER.md, the
+    TF Eager l2hmc example's ``compute_loss``): the networks are Variables;
+    one step draws z ~ N(0, I), proposes from the chains x and from z, and
+    minimises
+
+        l = mean(scale / d_x + scale / d_z - (d_x + d_z) / scale),
+        d = |x - x'|^2 * A(x' | x) + eps
+
+    (expected squared jump distance, both samples), then applies
+    ``v += -lr * grad``.  Staged mode mirrors the reference's mlp_train
+    pattern (stageflow/bench.py:131-144): the loss (both full transitions,
+    with the potential's tape gradient inside each leapfrog step) is one
+    staged function, the tape derives its staged backward — through every
+    leapfrog step, the networks and the MH step — and the update is a
+    second staged function."""
+
+    SCALE, EPS, LR = 0.1, 1e-4, 1e-3
+    gate_tol = 1e-5
+
+    def __init__(self, sf, batch: int, mode: str = "staged", seed: int = 0):
+        self.sf = sf
+        self.sampler = L2HMCSampler(sf, batch, "eager", seed=seed, trainable=True)
+        self.params = self.sampler.variables
+        s, b = self.sampler, batch
+
+        def forward_loss(x):
+            z = sf.random_normal((b, X_DIM))
+            x_out, x_acc, x_prop = s.propose(x)
+            _z_out, z_acc, z_prop = s.propose(z)
+
+            def jump(a, a_prop, acc):
+                d = sf.sub(a, a_prop)
+                return sf.add(sf.mul(sf.reduce_sum(sf.mul(d, d), axes=(1,)), acc), self.EPS)
+
+            dx, dz = jump(x, x_prop, x_acc), jump(z, z_prop, z_acc)
+            inv = sf.add(sf.div(1.0, dx), sf.div(1.0, dz))
+            per_chain = sf.sub(sf.mul(inv, self.SCALE), sf.div(sf.add(dx, dz), self.SCALE))
+            return sf.reduce_mean(per_chain), x_out
+
+        def apply_updates(*grads):
+            for v, g in zip(self.params, grads):
+                v.assign_add(sf.mul(g, -self.LR))
+
+        if mode == "staged":
+            self.forward_loss = sf.stage(forward_loss, name="l2hmc_train_loss")
+            self.apply_updates = sf.stage(apply_updates, name="l2hmc_train_apply")
+            self.staged_functions = [self.forward_loss, self.apply_updates]
+        else:
+            self.forward_loss = forward_loss
+            self.apply_updates = apply_updates
+            self.staged_functions = []
+        self.x = s.x
+
+    def step(self):
+        sf = self.sf
+        with sf.Tape() as t:
+            loss, x_out = self.forward_loss(self.x)
+        grads = t.gradient(loss, self.params)
+        self.apply_updates(*grads)
+        self.x = x_out
+        return loss
+
+    def run_iteration(self) -> float:
+        return float(self.step())
