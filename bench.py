@@ -592,6 +592,18 @@ def extras(sf, np, _native, plugins, l2hmc):
     c2["staged_over_eager"] = c2["staged"]["ops_per_sec"] / c2["eager"]["ops_per_sec"]
     out["c2_microbench"] = c2
     out["eager_launch_path"] = eager_path_extra(sf, np, _native, plugins)
+    # L2HMC training (the paper's L2HMC figure): ESJD loss over two full
+    # transitions, the tape's staged backward through every leapfrog step
+    tr_row = {}
+    for mode, n in (("staged", 10), ("eager", 2)):
+        sf.init_runtime(sf.RuntimeOptions(seed=1))
+        plugins.install()
+        tr = l2hmc.L2HMCTrain(sf, 200, mode, seed=0)
+        dt = _time_steps(tr.step, n, _native)
+        tr_row[mode] = {"ms_per_step": dt * 1e3, "samples_per_sec": 200 / dt}
+    tr_row["staged_over_eager"] = tr_row["eager"]["ms_per_step"] / tr_row["staged"]["ms_per_step"]
+    tr_row["chains"] = 200
+    out["l2hmc_training_200_chains"] = tr_row
     out["c4_resnet50_b32"] = resnet_extra(sf, np, _native)
     try:
         out["c5_resnet50_b256_1gpu"] = c5_extra(sf, _native, 0, 1, None)

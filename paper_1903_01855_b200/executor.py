@@ -27,6 +27,7 @@ from .errors import (CallbackError, DeadVariable, InputMismatch, KernelError, Mi
 from .graph import GraphFunction, Node
 from .kernels import KernelEnv, ordinal_of, relabel
 from .lowering import (FusedGroup, LOp, Lowerer, LV, PlanWriter, SLOT_CONST, SLOT_INPUT,
+                       alias_unwritten_reads,
                        SLOT_OUTPUT, SLOT_TEMP, cse, fuse, fuse_reductions, generate_group,
                        generate_reduce_group, pack_ew_step)
 from .runtime import current_context, get_runtime
@@ -147,7 +148,9 @@ class Program:
         from .rowfuse import plan_rows
 
         rowfuse.SM_COUNT = _sm_count(self.dev)
-        ops = cse(lw.ops) if fuse_enabled else lw.ops
+        keep = frozenset(id(v.root()) for v in self.out_vals)
+        ops = alias_unwritten_reads(lw.ops, keep) if fuse_enabled else lw.ops
+        ops = cse(ops) if fuse_enabled else ops
         self.has_rng = any(op.kind in ("rng", "dropout") for op in ops)
         keep = frozenset(id(v.root()) for v in self.out_vals)
         units = fuse(plan_rows(ops, keep) if fuse_enabled else ops, fuse_enabled)

@@ -421,6 +421,34 @@ def ew_expr(nm: str, args: List[str], ct: str) -> str:
     raise KernelError(f"fusion: no code for elementwise op {nm!r}")
 
 
+def alias_unwritten_reads(ops: List["LOp"], keep) -> List["LOp"]:
+    """read_variable of a variable no op of the program writes returns the
+    same value wherever it sits in the program's stateful chain: the read
+    becomes an alias of the variable's buffer instead of a snapshot copy, so
+    network weights stay uniform operands of the row programs (a trainable
+    L2HMC's 2,560 weight reads otherwise cut its transition into ~1,000
+    kernels).  A read whose value leaves the program (``keep``: outputs,
+    e.g. values saved for the backward) keeps its snapshot: the caller may
+    hold it across a later assignment) as a copy — an elementwise identity,
+    which the row planner treats as one more uniform op (the value is the
+    same at any point of the program)."""
+    written = {id(op.ins[0].root()) for op in ops
+               if op.kind in ("var_assign", "var_add") and op.ins}
+    out = []
+    for op in ops:
+        if op.kind == "var_read" and op.ins and id(op.ins[0].root()) not in written:
+            if id(op.outs[0]) in keep:
+                op.kind, op.name = "ew", "identity"
+            else:
+                o = op.outs[0]
+                o.kind = "alias"
+                o.base = op.ins[0]
+                o.producer = None
+                continue
+        out.append(op)
+    return out
+
+
 def c_literal(value, dtype: DType) -> str:
     if dtype is DType.float32:
         bits = struct.unpack("<I", struct.pack("<f", float(value)))[0]
