@@ -133,6 +133,7 @@ class Program:
         self.dev = ordinal_of(device)
         self.keep: List = []  # constant tensors whose buffers plans point at
         lw = Lowerer(self.dev, rng_mode)
+        lw.fold_captures = fuse_enabled and BAKE
         self.in_vals: List[LV] = []
         # inputs the program is specialised on (index -> weakref of the tensor)
         self.baked: Dict[int, "weakref.ref"] = {}
@@ -141,6 +142,7 @@ class Program:
             lv.index = i
             if fuse_enabled and bakeable(ph, v):
                 lv.vals = v.raw().reshape(-1)
+                lv.tensor = v  # (compile-time folding of nodes computed from it)
                 self.baked[i] = weakref.ref(v)
             self.in_vals.append(lv)
         self.out_vals = lw.lower_graph(gf, self.in_vals, libraries)

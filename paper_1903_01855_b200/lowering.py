@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _native, dtypes
 from .dtypes import DType
-from .errors import KernelError, MissingFunction
+from .errors import KernelError, MissingFunction, StageflowError
 from .tensor import Tensor
 
 # ---------------------------------------------------------------------------
@@ -98,6 +98,10 @@ class Lowerer:
         self.values: List[LV] = []
         self.ops: List[LOp] = []
         self.inputs: List[LV] = []
+        # fold nodes computed only from specialised captures and constants at
+        # compile time (Program sets it together with capture specialisation)
+        self.fold_captures = False
+        self.fold_max_numel = 1024
 
     def new(self, dtype, shape, kind) -> LV:
         v = LV(len(self.values), dtype, shape, kind)
@@ -115,10 +119,59 @@ class Lowerer:
             env[(i, 0)] = v
         for j, node in enumerate(gf.nodes):
             ins = [env[r] for r in node.inputs]
-            outs = self.lower_node(node, j, ins, libs, get_op_def(node.op))
+            op_def = get_op_def(node.op)
+            outs = self._fold(node, ins, op_def, gf.library) if self.fold_captures else None
+            if outs is None:
+                outs = self.lower_node(node, j, ins, libs, op_def)
             for k, o in enumerate(outs):
                 env[(n_in + j, k)] = o
         return [env[ref] for _, ref in gf.outputs]
+
+    @staticmethod
+    def _value_of(lv: LV):
+        """The immutable tensor behind a lowered value, if it has one (a
+        specialised capture or a constant; reshaped views included)."""
+        r = lv.root()
+        t = r.tensor
+        if t is None or r.kind not in ("const", "input"):
+            return None
+        if tuple(lv.shape) == tuple(t.shape):
+            return t
+        host = t._host.reshape(lv.shape) if t._host is not None else None
+        return Tensor._adopt(t.dtype, tuple(lv.shape), t.device, t._buf, host)
+
+    def _fold(self, node, ins, op_def, library):
+        """Constant-fold a node computed only from specialised captures and
+        constants, with the backend's own kernels (the reference's
+        constant_fold does the same for graph constants,
+        stageflow/graph.py:306-431; captured tensors are immutable, and a
+        program is compiled per capture identity): the sampler's chain-
+        independent values (weight transforms, time embeddings) become
+        literals of the row kernel and the per-call uniform kernel goes
+        away.  Returns the output values, or None when the node stays."""
+        if (op_def.stateful or node.op in ("constant", "call_function", "cond", "while_loop",
+                                           "host_call") or not ins
+                or any(dtypes.element_count(shape) > self.fold_max_numel
+                       for _, shape in node.out_specs if None not in tuple(shape))):
+            return None
+        vals = [self._value_of(x) for x in ins]
+        if any(v is None for v in vals):
+            return None
+        from . import executor
+
+        try:
+            res = executor.run_node_for_folding(node, vals, library)
+        except StageflowError:
+            return None
+        outs = []
+        for t in res:
+            v = self.new(t.dtype, t.shape, "const")
+            v.tensor = t
+            v.imm = _splat_value(t)
+            if t.dtype.is_float and 0 < t.size <= self.fold_max_numel:
+                v.vals = t.raw().reshape(-1)
+            outs.append(v)
+        return outs
 
     def _out(self, node, k=0) -> LV:
         dt, shape = node.out_specs[k]

@@ -80,6 +80,7 @@ def main():
     cf = pf._concrete_for(pf._bind(tuple(args), {}))
     gf = cf.graph
     lw = Lowerer(0, "device")
+    lw.fold_captures = executor.BAKE  # as Program does
     ins = []
     values = list(args) + cf.materialize_captured()
     for i, (ph, v) in enumerate(zip(gf.inputs, values)):
@@ -87,6 +88,7 @@ def main():
         lv.index = i
         if executor.bakeable(ph, v):  # as Program does
             lv.vals = v.raw().reshape(-1)
+            lv.tensor = v
         ins.append(lv)
     outs = lw.lower_graph(gf, ins, ())
     ops = cse(lw.ops)
