@@ -544,6 +544,10 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
   splits = (nk + per - 1) / per;
   const long long n_tiles = tiles * splits;
   const unsigned grid = (unsigned)(n_tiles < d->sm_count ? n_tiles : d->sm_count);
+  static const bool log_shapes = getenv("SF_GEMM_LOG") != nullptr;
+  if (log_shapes)
+    fprintf(stderr, "gemm_tc BN=%d amn=%d bmn=%d M=%lld N=%lld K=%lld tiles=%lld splits=%lld lo=%d%d\n",
+            BN, (int)AMN, (int)BMN, M, N, K, tiles, splits, lo_a_smem, lo_b_smem);
   float* out = c;
   float* work = nullptr;
   if (splits > 1)
