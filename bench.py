@@ -419,9 +419,13 @@ def run_ours(a, rank, world, dist):
     ms_per_step = total_s * 1e3 / a.steps
 
     # -- roofline of the dominant kernel: per-launch GPU time from plan events
+    # (the same L2 flush before every profiled step as in the timed region:
+    # the row kernel then refetches its code and weights as it does there)
     seg = prog.segments[0]
     seg.plan.profile(True)
-    for _ in range(3):
+    for _ in range(5):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
         sampler.step()
     stats = seg.plan.step_stats()
     seg.plan.profile(False)

@@ -103,6 +103,7 @@ REROLL = __import__("os").environ.get("SF_REROLL", "1") == "1"
 
 class RowProgram:
     __slots__ = ("ops", "batch", "gen", "uniform_only", "block", "replicas", "cpool", "teams",
+                 "team_width", "min_blocks", "row_threads",
                  "rows_per_cta", "dyn_smem")
 
     def __init__(self, batch: int):
@@ -120,6 +121,9 @@ class RowProgram:
         # the program for the same 64 chains (find_teams), or None
         self.teams = None
         self.rows_per_cta = 128  # chains per CTA (set by code generation)
+        self.team_width = 0  # threads per team of a team-split kernel
+        self.min_blocks = 0  # CTAs per SM the launch bounds ask for
+        self.row_threads = 128  # threads of a CTA that own chains
         self.dyn_smem = 0  # dynamic shared memory bytes of the kernel
 
 
@@ -168,6 +172,7 @@ def _synthetic(dtype, shape, kind: str, base: Optional[LV] = None) -> LV:
 
 MIN_REPS = 3
 MIN_PERIOD = 4
+PHASE_SHIFTS = 8  # block starts tried within the first block of a repeat
 
 
 def _sig(op: LOp, planner) -> tuple:
@@ -209,16 +214,31 @@ def reroll(ops: List[LOp], planner, users: Dict[int, List[LOp]], keep: set) -> L
                 cands.append(((reps - 1) * p, p, s, reps))
     cands.sort(key=lambda c: (-c[0], c[1]))
     for _score, p, s, reps in cands[:40]:
-        for front in range(3):
-            for back in range(3):
-                m = reps - front - back
-                if m < MIN_REPS:
+        # spans that start 0-2 whole blocks in, or a few ops into a block (the
+        # first block of a traced loop often reads a value computed before
+        # the loop where later blocks compute it themselves; starting the
+        # blocks one op later turns that operand into a carried one), with
+        # as many blocks as the periodic run from that start allows
+        eq = seq[:-p] == seq[p:]
+        tried, attempts = set(), []
+        for shift in range(min(p, PHASE_SHIFTS)):
+            for front in range(3):
+                s0 = s + front * p + shift
+                if s0 >= len(eq):
                     continue
-                s0 = s + front * p
-                loop = _make_loop(ops[s0:s0 + m * p], p, m, planner, users, keep)
-                if loop is not None:
-                    return (reroll(ops[:s0], planner, users, keep) + [loop]
-                            + reroll(ops[s0 + m * p:], planner, users, keep))
+                stop = np.flatnonzero(~eq[s0:])
+                run = int(stop[0]) if len(stop) else len(eq) - s0
+                for back in range(3):
+                    m = 1 + run // p - back
+                    if m >= MIN_REPS and (m, s0) not in tried:
+                        tried.add((m, s0))
+                        attempts.append((-m, s0))
+        for neg_m, s0 in sorted(attempts)[:64]:
+            m = -neg_m
+            loop = _make_loop(ops[s0:s0 + m * p], p, m, planner, users, keep)
+            if loop is not None:
+                return (reroll(ops[:s0], planner, users, keep) + [loop]
+                        + reroll(ops[s0 + m * p:], planner, users, keep))
     return list(ops)
 
 
@@ -808,7 +828,11 @@ class _Gen:
             rv = self.rowv[rep]
             st = " ".join(f"(({ct}*)a.p[@O{o.id}@])[{rv if w == 1 else f'{rv} * {w} + {j}'}]"
                           f" = {nm};" for j, nm in enumerate(names))
-            lines.append(st if rep == 0 else f"if (v{rv}) {{ {st} }}")
+            if rep > 0:
+                st = f"if (v{rv}) {{ {st} }}"
+            elif LOOP_SYNC and not self.rp.uniform_only and self.rp.teams is None:
+                st = f"if (live) {{ {st} }}"
+            lines.append(st)
 
     # -- operand access -------------------------------------------------------------
     def _input(self, x: LV) -> None:
@@ -905,7 +929,7 @@ class _Gen:
         pos = -(-self.pool_size // 16) * 16
         self.pool[name] = (pos, size, ct, width)
         self.pool_size = pos + max(1, size * len(slots)) * width
-        head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= 128 else
+        head = (f"if (const int q = threadIdx.x; q < {n}) " if n <= self.rp.block else
                 f"for (int q = threadIdx.x; q < {n}; q += blockDim.x) ")
         for i, k in enumerate(slots):
             dst = f"smem_pool + {pos + i * size * width} + {width} * ({off})"
@@ -1183,6 +1207,17 @@ class _Gen:
                 self._emit_uniform_loop(op)
             else:
                 self._emit_rowed(op, L)
+                self._maybe_sync(op)
+
+    def _maybe_sync(self, op) -> None:
+        """With LOOP_SYNC: a CTA barrier after about SYNC_EVERY scalar ops of
+        straight-line (or loop-body) code."""
+        if not LOOP_SYNC or SYNC_EVERY <= 0 or self.rp.uniform_only or self.rp.teams is not None:
+            return
+        self.since_sync = getattr(self, "since_sync", 0) + _op_cost(op, self.P)
+        if self.since_sync >= SYNC_EVERY:
+            self.since_sync = 0
+            self.body.append("    __syncthreads();")
 
     def _emit_teams(self) -> None:
         """Team 0 / team 1 bodies and the join body (see find_teams): team 0
@@ -1208,7 +1243,8 @@ class _Gen:
                         self.team_decls.append(f"  {ct} tk{lv.id}_{j};")
                         self.body.append(f"    tk{lv.id}_{j} = {nm};")
                     else:
-                        self.team_decls.append(f"  __shared__ {ct} xf{lv.id}_{j}[64];")
+                        self.team_decls.append(
+                            f"  __shared__ {ct} xf{lv.id}_{j}[{self.rp.team_width}];")
                         self.body.append(f"    xf{lv.id}_{j}[lid] = {nm};")
             bodies.append(self.body)
         self.body, self.scope_rows = [], set()
@@ -1272,10 +1308,15 @@ class _Gen:
             pre.append(" ".join(f"{ct} {nm} = ({ct})0;" for names in per_rep for nm in names))
             exp_names.append(per_rep)
         pre.append(f"#pragma unroll 1\n    for (int it = 0; it < {lp.m}; ++it) {{")
+        if LOOP_SYNC and self.rp.teams is None:
+            pre.append("__syncthreads();")
         self.body.append(self._fill("    " + "\n    ".join(pre)))
         self.in_loop = True
+        self.since_sync = 0
         for op in lp.body:
             self._emit_rowed(op, self.P.layout_of(op.outs[0]))
+            self._maybe_sync(op)
+        self.since_sync = 0
         self.in_loop = False
         post = []
         for (e, b), per_rep in zip(lp.exports, exp_names):
@@ -1511,6 +1552,22 @@ class _Gen:
                     if xpack:
                         for c in range(n):
                             per_rep[rep][c] = f"{base}_{c}x.{'xy'[rep]}"
+            elif xpack:
+                # two chains per thread, weights specialised as literals:
+                # output j of both chains in one float2, FFMA2 with the weight
+                # as a broadcast immediate (one instruction per weight for two
+                # chains; the same sequential-k FMA chain per lane)
+                xps = [self._pair(xs_rep[0][kk], xs_rep[1][kk], lines) for kk in range(kk_n)]
+                for j in range(n):
+                    acc = "make_float2(0.0f, 0.0f)"
+                    for kk in range(kk_n):
+                        wv = self._pair(self.uni_elem(b, kk * n + j), self.uni_elem(b, kk * n + j),
+                                        lines)
+                        acc = f"sf::fma2({xps[kk]}, {wv}, {acc})"
+                    pn = f"{base}_{j}x"
+                    lines.append(f"const float2 {pn} = {acc};")
+                    self.f2vars.add(pn)
+                    per_rep[0][j], per_rep[1][j] = pn + ".x", pn + ".y"
             else:
                 for j in range(n):
                     for rep in range(self.R):
@@ -1569,7 +1626,64 @@ def generate_rowprog(rp: RowProgram, planner: RowPlanner, needed: set):
     return rp.gen
 
 
+# Row-kernel grid: "balanced" spreads the chains evenly over a grid that is a
+# whole multiple of the SM count (each CTA gets ceil(batch / CTAs) chains, so
+# every SM carries the same number of chains); "legacy" = 128 (64 per team)
+# chains per CTA, whatever the remainder.  Measured on B200, L2HMC 1e5 chains:
+# 782 legacy CTAs put 6 CTAs on 42 SMs and 5 on the rest (ncu: SM active
+# cycles only 80% of elapsed).
+# (B200, L2HMC 1e5 chains, device time per transition, warm L2: legacy
+# 128-chain CTAs 137 us; balanced 256-thread CTAs 120 us; balanced with one
+# 704-thread CTA per SM and LOOP_SYNC 108 us.)
+ROW_GRID = __import__("os").environ.get("SF_ROW_GRID", "balanced")
+# a CTA barrier at the top of every re-rolled loop iteration: keeps the
+# CTA's warps within one loop body of each other (shared instruction fetch)
+# (1e5 chains: 704-thread CTAs 119.7 -> 108 us; 256-thread 119.7 -> 112 us;
+# extra barriers in straight-line code every 150-600 scalar ops: no gain)
+LOOP_SYNC = __import__("os").environ.get("SF_ROW_LOOPSYNC", "1") == "1"
+SYNC_EVERY = int(__import__("os").environ.get("SF_ROW_SYNC_EVERY", "0"))
+# most threads per CTA of a balanced row kernel (704 = 22 warps: 1e5 chains
+# as one CTA per SM at <= 93 registers per thread)
+ROW_CTA_THREADS = int(__import__("os").environ.get("SF_ROW_CTA_THREADS", "704"))
+
+
+def _geometry(rp: RowProgram, teams: bool) -> None:
+    """Sets rp.rows_per_cta, rp.row_threads, rp.block, rp.team_width and
+    rp.min_blocks (the launch bounds' CTAs per SM)."""
+    rp.team_width = 0
+    rp.min_blocks = 0
+    if rp.uniform_only:
+        rp.rows_per_cta = 128
+        return
+    R = rp.replicas
+    b = rp.batch
+    if teams:
+        # small batches: 64 chains per CTA spreads the latency-bound chains
+        # over as many SMs as possible
+        rpc = 64
+    elif ROW_GRID == "balanced" and b >= 32 * SM_COUNT * R:
+        tmax = ROW_CTA_THREADS // R
+        per_sm = -(-(-(-b // (tmax * R))) // SM_COUNT)
+        rpc = -(-b // (SM_COUNT * per_sm))
+    else:
+        rpc = 128 * R
+    per_sm = -(-(-(-b // rpc)) // SM_COUNT)
+    rp.rows_per_cta = rpc
+    rp.row_threads = -(-rpc // R)          # threads with a chain (replica 0's rows)
+    width = 32 * -(-rp.row_threads // 32)  # threads per team (or per CTA)
+    rp.block = 2 * width if teams else width
+    if teams:
+        rp.team_width = width
+    # fit the whole batch in ONE wave when a register cap allows it (and
+    # leaves ~80 registers per chain): with 1e5 chains in 128-chain CTAs,
+    # 6 CTAs per SM need <= 80 registers (an 87-register kernel ran 5/SM
+    # and spilled 42 CTAs into a second wave)
+    if 2 <= per_sm <= 7 and rp.block * per_sm * 80 * R <= 65536:
+        rp.min_blocks = per_sm
+
+
 def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
+    _geometry(rp, rp.teams is not None and not rp.uniform_only and rp.replicas == 1)
     g = _Gen(rp, planner, needed)
     g.emit()
     stores = []
@@ -1595,17 +1709,10 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         g.team_bodies = bodies
     n_ptr = k0 + len(g.outs)
     n_rng = max(1, len(g.rng_ops))
-    rp.block = g.block if rp.uniform_only else 128
-    rp.rows_per_cta = 64 if rp.teams is not None else 128 * rp.replicas
-    mb = MIN_BLOCKS
-    if not rp.uniform_only and mb == 0:
-        # fit the whole batch in ONE wave when a register cap allows it: with
-        # 1e5 chains, 782 CTAs need 6 per SM, i.e. <= 80 registers (an 87-
-        # register kernel ran 5/SM and spilled 42 CTAs into a second wave)
-        per_sm = -(-(-(-rp.batch // rp.rows_per_cta)) // SM_COUNT)
-        if 2 <= per_sm <= 7:
-            mb = per_sm
-    bounds = str(rp.block) if rp.uniform_only or mb == 0 else f"128, {mb}"
+    if rp.uniform_only:
+        rp.block = g.block
+    mb = MIN_BLOCKS or (0 if rp.uniform_only else rp.min_blocks)
+    bounds = str(rp.block) if rp.uniform_only or mb == 0 else f"{rp.block}, {mb}"
     src = [f"struct Params {{ void* p[{max(1, n_ptr)}]; long long rows; "
            f"unsigned long long seed; unsigned long long off[{n_rng}]; }};",
            f"extern \"C\" __global__ void __launch_bounds__({bounds}) KNAME(const "
@@ -1637,9 +1744,10 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr
     if rp.teams is not None:
         # two teams of two warps over the CTA's 64 chains (find_teams)
-        src.append("  const int team = threadIdx.x >> 6, lid = threadIdx.x & 63;")
-        src.append("  const long long r = (long long)blockIdx.x * 64 + lid;")
-        src.append("  const bool live = r < a.rows;")
+        tw, rpc = rp.team_width, rp.rows_per_cta
+        src.append(f"  const int team = threadIdx.x >= {tw}, lid = threadIdx.x - team * {tw};")
+        src.append(f"  const long long r = (long long)blockIdx.x * {rpc} + lid;")
+        src.append(f"  const bool live = lid < {rpc} && r < a.rows;")
         src += g.team_decls
         src.append("  if (live && team == 0) {")
         src += g.team_bodies[0]
@@ -1654,11 +1762,29 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
         return name, source, list(g.ext), list(g.outs), [c for _, c in g.rng_ops], n_ptr
     # R chains per thread (rows r + 128 k of the CTA's 128 R rows; a replica
     # past the end computes on the last row and does not store)
-    src.append(f"  const long long r = (long long)blockIdx.x * {128 * g.R} + threadIdx.x;")
-    src.append("  if (r >= a.rows) return;")
+    # replica k of a thread owns row r + k T of its CTA's rows (T = threads
+    # with a chain); a replica past the CTA's rows computes on row r and does
+    # not store
+    rpc, T = rp.rows_per_cta, rp.row_threads
+    if LOOP_SYNC:
+        # every thread reaches the per-iteration barriers: a thread without
+        # a chain computes on its CTA's first row and does not store
+        src.append(f"  const long long r0 = (long long)blockIdx.x * {rpc} + threadIdx.x;")
+        src.append(f"  const bool live = threadIdx.x < {T} && r0 < a.rows;")
+        src.append(f"  const long long r = live ? r0 : (long long)blockIdx.x * {rpc};")
+    else:
+        src.append(f"  const long long r = (long long)blockIdx.x * {rpc} + threadIdx.x;")
+    if LOOP_SYNC:
+        pass
+    elif T < rp.block:
+        src.append(f"  if (threadIdx.x >= {T} || r >= a.rows) return;")
+    else:
+        src.append("  if (r >= a.rows) return;")
+    if g.R > 1:
+        src.append(f"  const long long rend = min((long long)blockIdx.x * {rpc} + {rpc}, a.rows);")
     for k in range(1, g.R):
-        src.append(f"  const bool vrq{k} = r + {128 * k} < a.rows;")
-        src.append(f"  const long long rq{k} = vrq{k} ? r + {128 * k} : a.rows - 1;")
+        src.append(f"  const bool vrq{k} = r + {T * k} < rend;")
+        src.append(f"  const long long rq{k} = vrq{k} ? r + {T * k} : r;")
     src.append("  {")
     src += g.body
     if stores:
