@@ -21,6 +21,8 @@ A GraphFunction is compiled once per (device, concrete input signature):
 from __future__ import annotations
 
 import hashlib
+import os
+import re
 import struct
 from typing import Any, Dict, List, Optional, Sequence, Tuple
 
@@ -723,6 +725,17 @@ def fuse_reductions(units: List[Any]) -> List[Any]:
     return out
 
 
+RED_UNROLL = int(os.environ.get("SF_RED_UNROLL", "4"))
+
+
+def _unroll_rename(line: str, u: int) -> str:
+    """An operand-load line of _x4_parts for unrolled row u (its index
+    variables i/t and its in*_s / in*_v names suffixed with u)."""
+    line = re.sub(r"\b(in\d+_[sv])\b", rf"\g<1>{u}", line)
+    line = re.sub(r"\bi\b", f"i{u}", line)
+    return re.sub(r"\bt\b", f"t{u}", line)
+
+
 def generate_reduce_group(group: FusedGroup, needed_after: set, sm_count: int):
     """CUDA source of a fused group that also folds column reductions of its
     values (see fuse_reductions).  Thread (tx, l) of a block owns 4 adjacent
@@ -774,14 +787,32 @@ def generate_reduce_group(group: FusedGroup, needed_after: set, sm_count: int):
            f"  const long long g0 = j * {chunk};",
            f"  const long long len = {r_rows}LL - g0 < {chunk} ? {r_rows}LL - g0 : {chunk};"]
     src += [f"  float4 acc{k} = make_float4(0.f, 0.f, 0.f, 0.f);" for k in range(k_red)]
+    # RED_UNROLL rows of a lane per iteration: all their operand loads are
+    # issued first, then the rows are computed and folded in row order (the
+    # CRO is unchanged; a 1024-row chunk is 32 dependent load rounds without
+    # this, which left the late layers' reductions latency-bound)
+    U = RED_UNROLL
     src += [f"  if (c0 < {c} && tl < len) {{",
             "    bool first = true;",
-            f"    for (long long row = g0 + tl; row < g0 + len; row += 32) {{",
-            f"    const long long i = row * {c} + c0;",
-            "    const long long t = i >> 2;"]
-    src += lines + decl
-    src += ["#pragma unroll", "    for (int e = 0; e < 4; ++e) {"] + body + ["    }"]
-    src += stores + fold + ["      first = false;", "    }", "  }"]
+            f"    for (long long row = g0 + tl; row < g0 + len; row += {32 * U}) {{"]
+    loaded = []
+    for u in range(U):
+        src += [f"    const long long row{u} = min(row + {32 * u}LL, g0 + len - 1);",
+                f"    const long long i{u} = row{u} * {c} + c0;",
+                f"    const long long t{u} = i{u} >> 2;"]
+        for ln in lines:
+            m = re.match(r"\s*const (\S+) (in\d+_[sv]) =", ln)
+            if m and u == 0:
+                loaded.append((m.group(1), m.group(2)))
+            src.append(_unroll_rename(ln, u))
+    for u in range(U):
+        guard = "" if u == 0 else f"if (row + {32 * u} < g0 + len) "
+        src += [f"    {guard}{{", f"    const long long i = i{u}, t = t{u};"]
+        src += [f"    const {ty} {nm} = {nm}{u};" for ty, nm in loaded]
+        src += decl
+        src += ["#pragma unroll", "    for (int e = 0; e < 4; ++e) {"] + body + ["    }"]
+        src += stores + fold + ["      first = false;", "    }"]
+    src += ["    }", "  }"]
     for k in range(k_red):
         src += [f"  acc_s[{k}][tl][tx * 4 + 0] = acc{k}.x; acc_s[{k}][tl][tx * 4 + 1] = acc{k}.y;",
                 f"  acc_s[{k}][tl][tx * 4 + 2] = acc{k}.z; acc_s[{k}][tl][tx * 4 + 3] = acc{k}.w;"]

@@ -27,6 +27,20 @@ for b in [int(x) for x in sys.argv[1:]] or [200]:
         s.step()
     _native.sync(0)
     n = 50
+    if os.environ.get("FLUSH") == "1":
+        # as bench.py times the headline: 256 MiB written between steps
+        buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+        ts = []
+        for _ in range(n):
+            with torch.cuda.stream(stream):
+                buf.fill_(1.0)
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+            s.step()
+            a1.record(stream)
+            ts.append((a0, a1))
+        _native.sync(0)
+        out[f"{b}_flushed"] = {"device_us": sum(a.elapsed_time(c) for a, c in ts) * 1e3 / n}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     t = time.perf_counter()
