@@ -382,9 +382,23 @@ __global__ void splitk_reduce_x4(const float4* __restrict__ W, float4* __restric
                                  long long mn4, int splits) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mn4; i += stride) {
-    float4 acc = W[i];
-    for (int s = 1; s < splits; ++s) {
-      const float4 v = W[(long long)s * mn4 + i];
+    // partials added in split order; 8 splits' loads in flight per round
+    float4 acc = __ldcs(W + i);
+    int s = 1;
+    for (; s + 8 <= splits; s += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(W + (long long)(s + u) * mn4 + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x = acc.x + v[u].x;
+        acc.y = acc.y + v[u].y;
+        acc.z = acc.z + v[u].z;
+        acc.w = acc.w + v[u].w;
+      }
+    }
+    for (; s < splits; ++s) {
+      const float4 v = __ldcs(W + (long long)s * mn4 + i);
       acc.x = acc.x + v.x;
       acc.y = acc.y + v.y;
       acc.z = acc.z + v.z;

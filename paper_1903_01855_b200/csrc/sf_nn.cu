@@ -355,6 +355,51 @@ __global__ void maxpool_kernel(const T* __restrict__ x, T* __restrict__ y, ConvG
   }
 }
 
+// float32, C % 4 == 0, fewer than 2^31 elements: a thread owns 4 channels of
+// one output pixel (float4 loads, 32-bit index math); each lane applies
+// maxpool_kernel's rule (first maximum in kh, kw order; the first NaN wins),
+// so the result is bit-identical.  With write_argmax it stores the window
+// position of that maximum instead (maxpool_argmax_kernel's rule).
+template <bool ARGMAX>
+__global__ void __launch_bounds__(256) maxpool_f32x4_kernel(const float* __restrict__ x,
+                                                            float* __restrict__ y,
+                                                            signed char* __restrict__ am,
+                                                            ConvGeom g) {
+  const int C4 = (int)g.c / 4, W = (int)g.w, H = (int)g.h, WO = (int)g.wo, HO = (int)g.ho;
+  const int S = (int)g.s, P = (int)g.p, KH = (int)g.kh, KW = (int)g.kw;
+  const int total = (int)(g.n * g.ho * g.wo) * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4, t = i / C4;
+    const int ow = t % WO, t2 = t / WO;
+    const int oh = t2 % HO, n = t2 / HO;
+    float b[4] = {0.f, 0.f, 0.f, 0.f};
+    int bi[4] = {-1, -1, -1, -1};
+    for (int kh = 0; kh < KH; ++kh) {
+      const int ih = oh * S - P + kh;
+      if (ih < 0 || ih >= H) continue;
+      for (int kw = 0; kw < KW; ++kw) {
+        const int iw = ow * S - P + kw;
+        if (iw < 0 || iw >= W) continue;
+        const float4 v4 = reinterpret_cast<const float4*>(x)[((n * H + ih) * W + iw) * C4 + c4];
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v = vv[e];
+          if (bi[e] < 0 || v > b[e] || (v != v && b[e] == b[e])) {
+            b[e] = v;
+            bi[e] = kh * KW + kw;
+          }
+        }
+      }
+    }
+    if (ARGMAX)
+      reinterpret_cast<char4*>(am)[i] = make_char4((signed char)bi[0], (signed char)bi[1],
+                                                   (signed char)bi[2], (signed char)bi[3]);
+    else
+      reinterpret_cast<float4*>(y)[i] = make_float4(b[0], b[1], b[2], b[3]);
+  }
+}
+
 template <class T>
 __device__ __forceinline__ bool is_argmax(const T* x, const ConvGeom& g, long long n, long long oh,
                                           long long ow, long long c, long long h, long long w) {
@@ -717,7 +762,11 @@ int sf_maxpool2d(int dev, int dtype, const int64_t* g8, const void* x, void** y)
   count_launch(dev);
   return by_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    maxpool_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)x, (T*)*y, g);
+    if (std::is_same<T, float>::value && g.c % 4 == 0 && g.n * g.h * g.w * g.c < (1ll << 31))
+      maxpool_f32x4_kernel<false><<<grid_for_n(d, total / 4), 256, 0, d->stream>>>(
+          (const float*)x, (float*)*y, nullptr, g);
+    else
+      maxpool_kernel<T><<<grid_for_n(d, total), 256, 0, d->stream>>>((const T*)x, (T*)*y, g);
     SF_CHECK_CUDA(cudaGetLastError());
     return SF_OK;
   });
@@ -738,7 +787,11 @@ int sf_maxpool2d_grad(int dev, int dtype, const int64_t* g8, const void* x, cons
     count_launch(dev, 2);
     const int st = by_dtype(dtype, [&](auto t) {
       using T = decltype(t);
-      maxpool_argmax_kernel<T><<<grid_for_n(d, outs), 256, 0, d->stream>>>((const T*)x, am, g);
+      if (std::is_same<T, float>::value && g.c % 4 == 0)
+        maxpool_f32x4_kernel<true><<<grid_for_n(d, outs / 4), 256, 0, d->stream>>>(
+            (const float*)x, nullptr, am, g);
+      else
+        maxpool_argmax_kernel<T><<<grid_for_n(d, outs), 256, 0, d->stream>>>((const T*)x, am, g);
       if (std::is_same<T, float>::value && g.c % 4 == 0)
         maxpool_gather_f32x4_kernel<<<grid_for_n(d, total / 4), 256, 0, d->stream>>>(
             am, (const float*)dy, (float*)*dx, g);

@@ -81,6 +81,16 @@ def test_maxpool_grad_vectorised_vs_oracle(shape, k, s, p):
                                rtol=1e-6, atol=1e-6)
 
 
+def test_maxpool_vectorised_nan_first_wins():
+    """NaNs in the 4-channel forward kernel: a window holding a NaN yields
+    NaN (np.maximum's propagation, the oracle); lanes without NaNs are exact."""
+    rng = np.random.default_rng(5)
+    x = rng.integers(-3, 3, size=(2, 9, 9, 8)).astype(np.float32)
+    x[rng.random(x.shape) < 0.1] = np.nan
+    y = nn.max_pool(sf.constant(x), 3, 2, 1)
+    np.testing.assert_array_equal(y.numpy(), nn_np.max_pool(x, 3, 2, 1))
+
+
 def test_maxpool_and_xent_vs_oracle():
     rng = np.random.default_rng(1)
     x = rng.standard_normal((2, 9, 9, 3)).astype(np.float32)
