@@ -155,9 +155,10 @@ __global__ void __launch_bounds__(320, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap tAhi,
                        const __grid_constant__ CUtensorMap tAlo,
                        const __grid_constant__ CUtensorMap tBhi,
-                       const __grid_constant__ CUtensorMap tBlo, float* __restrict__ C, int M,
+                       const __grid_constant__ CUtensorMap tBlo,
+                       const __grid_constant__ CUtensorMap tC, float* __restrict__ C, int M,
                        int N, int K, int kb_per_split, int tiles_n, int tiles_mn, int n_tiles,
-                       int lo_a_smem, int lo_b_smem) {
+                       int lo_a_smem, int lo_b_smem, int tma_c) {
   constexpr int TC_STAGES = TcStages<BN>::n;  // shadows the default ring depth
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4, B_BYTES = BN * TC_BK * 4;
   constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
@@ -327,6 +328,64 @@ __global__ void __launch_bounds__(320, 1)
     // epilogue warps 2..5: TMEM lane quarter q = warp % 4 -> tile rows [32q, 32q + 32)
     const int q = warp & 3;
     int i = 0;
+    if (tma_c) {
+      // 32x32 sub-tiles: tcgen05.ld (thread = row), registers -> a 128B-
+      // swizzled 4 KB smem box (two per warp, alternating), TMA store of the
+      // box (rows >= M / columns >= N clipped by the tensor map); the TMEM
+      // buffer is released as soon as its last columns are in registers
+      uint8_t* ebuf = smem + TC_STAGES * STAGE_BYTES + 1024 + q * 8192;
+      uint32_t chunk = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int z = t / tiles_mn, mn = t - z * tiles_mn;
+        const int m0 = (mn / tiles_n) * TC_BM, n0 = (mn % tiles_n) * BN;
+        const int b = i & 1;
+        mbar_wait(&acc_full[b], (uint32_t)(i >> 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32, ++chunk) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+              "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, "
+              "%26, %27, %28, %29, %30, %31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),
+                "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c0 + 32 >= BN) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+          }
+          uint8_t* box = ebuf + (chunk & 1u) * 4096;
+          // the store issued from this box two chunks ago must have read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          const uint32_t rowa = smem_u32(box) + (uint32_t)lane * 128u;
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             rowa + (uint32_t)((v ^ (lane & 7)) * 16)),
+                         "r"(r[4 * v]), "r"(r[4 * v + 1]), "r"(r[4 * v + 2]), "r"(r[4 * v + 3])
+                         : "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                ::"l"(&tC), "r"(n0 + c0), "r"(m0 + q * 32), "r"(z), "r"(smem_u32(box))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else {
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int z = t / tiles_mn, mn = t - z * tiles_mn;
       const int m0 = (mn / tiles_n) * TC_BM, n0 = (mn % tiles_n) * BN;
@@ -366,6 +425,7 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
+    }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -511,6 +571,29 @@ static int encode_map(CUtensorMap* map, const float* ptr, long long rows, long l
   return SF_OK;
 }
 
+// GEMM output (Z split slices of M x N, row-major) for the TMA-store
+// epilogue: 32 x 32 boxes, 128B swizzle (the epilogue's smem box layout)
+static int encode_out_map(CUtensorMap* map, float* ptr, long long M, long long N, long long Z) {
+  if (!drv.tensorMapEncodeTiled) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SF_ERR_CUDA;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)Z};
+  const cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)(M * N * 4)};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  SF_CHECK_CU(drv.tensorMapEncodeTiled(
+      map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ptr, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  return SF_OK;
+}
+
+static bool no_tma_store() {
+  static const bool off = getenv("SF_GEMM_NO_TMA_STORE") != nullptr;
+  return off;
+}
+
 // ak / bk: the contraction extent each operand actually stores (<= K; the
 // TMA boxes zero-fill beyond it).  K-major: the row length (leading
 // dimension); MN-major: the number of rows.
@@ -537,7 +620,9 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
     SF_TRY(encode_map(&tb, bhi, N, bk, BN));
     SF_TRY(encode_map(&tbl, blo, N, bk, BN));
   }
-  const int smem = TcStages<BN>::n * (2 * TC_BM * TC_BK * 4 + 2 * BN * TC_BK * 4) + 1024 + 256;
+  // + 4 epilogue warps x two 4 KB output boxes (TMA-store epilogue)
+  const int smem = TcStages<BN>::n * (2 * TC_BM * TC_BK * 4 + 2 * BN * TC_BK * 4) + 1024 + 1024 +
+                   4 * 8192;
   static bool configured[64] = {};
   if (!configured[d->id]) {
     SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN, AMN, BMN>,
@@ -567,9 +652,18 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
   if (splits > 1)
     SF_TRY(d->alloc.alloc(d->id, sizeof(float) * (size_t)(splits * M * N), (void**)&work));
   if (work) out = work;
+  // output through TMA stores when the rows are 16-byte multiples
+  CUtensorMap tc;
+  int tma_c = 0;
+  if (N % 4 == 0 && (uintptr_t)out % 16 == 0 && !no_tma_store()) {
+    SF_TRY(encode_out_map(&tc, out, M, N, splits));
+    tma_c = 1;
+  } else {
+    tc = ta;  // unused
+  }
   gemm_tc_persistent<BN, AMN, BMN><<<grid, 320, smem, d->stream>>>(
-      ta, tal, tb, tbl, out, (int)M, (int)N, (int)K, (int)per, (int)tiles_n, (int)tiles,
-      (int)n_tiles, lo_a_smem, lo_b_smem);
+      ta, tal, tb, tbl, tc, out, (int)M, (int)N, (int)K, (int)per, (int)tiles_n, (int)tiles,
+      (int)n_tiles, lo_a_smem, lo_b_smem, tma_c);
   if (splits == 1) {
     count_launch(d->id);
     SF_CHECK_CUDA(cudaGetLastError());
