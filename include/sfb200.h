@@ -227,6 +227,16 @@ int sf_gemm_tf32x3(int dev, int64_t m, int64_t n, int64_t k, const void* a_hi, c
 int sf_gemm_tf32x3_ex(int dev, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn, int64_t ak,
                       int64_t bk, const void* a_hi, const void* a_lo, const void* b_hi,
                       const void* b_lo, void** c);
+/* Implicit-GEMM convolution on tcgen05 (3xTF32), NHWC float32:
+ * out[n*ho*wo, co] = im2col(x) . W with W (kh*kw*c, co) row-major and
+ * g8 = {N, H, W, C, KH, KW, stride, pad}; the im2col rows are gathered into
+ * shared memory by the GEMM itself (never materialised).  Requires
+ * C % 32 == 0 and co % 4 == 0 (else SF_ERR_INVALID).  Bit-identical to
+ * sf_im2col + sf_gemm_tf32x3_ex.  Replaces the im2col + GEMM of the
+ * reference's conv2d plugin kernel (oracle/ref_plugins.py, the numpy
+ * restatement of the C4 workload's convolution). */
+int sf_conv2d_tc(int dev, const int64_t* g8, int64_t co, const void* x, const void* w,
+                 void** out);
 /* hi/lo split of an fp32 (rows x cols) matrix; transpose=1 writes the
  * (cols x ldo) transpose with rows zero-padded to ldo.  Without transpose,
  * hi may be NULL: the tensor cores ignore an fp32 operand's low 13 mantissa

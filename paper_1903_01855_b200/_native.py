@@ -90,6 +90,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "sf_im2col": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP, _PVP]),
         "sf_col2im": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP, _PVP]),
         "sf_maxpool2d": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP, _PVP]),
+        "sf_conv2d_tc": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, _I64, _VP, _VP, _PVP]),
         "sf_maxpool2d_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _VP,
                                               _VP, _PVP]),
         "sf_softmax_xent": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _I64, _VP, _VP,
@@ -158,7 +159,7 @@ EXPORTED_SYMBOLS = (
     "sf_plan_create", "sf_plan_run", "sf_plan_info", "sf_plan_destroy", "sf_launch_count",
     "sf_plan_profile", "sf_plan_step_stats", "sf_im2col", "sf_col2im", "sf_maxpool2d",
     "sf_maxpool2d_grad", "sf_softmax_xent", "sf_softmax_xent_grad", "sf_gemm_tf32x3",
-    "sf_gemm_tf32x3_ex",
+    "sf_gemm_tf32x3_ex", "sf_conv2d_tc",
     "sf_split_tf32", "sf_im2col_split", "sf_while_create", "sf_cond_create", "sf_graph_create",
     "sf_while_buffer",
     "sf_while_capture_begin", "sf_while_set_cond", "sf_while_capture_end", "sf_while_launch",

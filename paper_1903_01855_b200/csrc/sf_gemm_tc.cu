@@ -150,7 +150,17 @@ __device__ __forceinline__ float4 tf32_lo4(float4 v, float4* h) {
 // over unchanged), halving the operand bytes the TMA moves per k-block and
 // making the separate split pass unnecessary.  The MMA issuer then waits on
 // the converters' barrier instead of the TMA's.
-template <int BN, bool AMN, bool BMN>
+// Implicit-GEMM convolution geometry (GATHER): A = im2col(x) of an NHWC
+// input with C % 32 == 0 is never materialised — the producer warp gathers
+// each 128-row x 32-k A tile (32 channels of one filter tap for 128 output
+// pixels) straight from x with 16-byte cp.async into the same 128B-swizzled
+// layout the TMA would have written (zero-filled outside the image).
+struct GatherGeom {
+  const float* x;
+  int h, w, c, kw, s, p, wo, howo;
+};
+
+template <int BN, bool AMN, bool BMN, bool GATHER = false>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_persistent(const __grid_constant__ CUtensorMap tAhi,
                        const __grid_constant__ CUtensorMap tAlo,
@@ -158,7 +168,7 @@ __global__ void __launch_bounds__(320, 1)
                        const __grid_constant__ CUtensorMap tBlo,
                        const __grid_constant__ CUtensorMap tC, float* __restrict__ C, int M,
                        int N, int K, int kb_per_split, int tiles_n, int tiles_mn, int n_tiles,
-                       int lo_a_smem, int lo_b_smem, int tma_c) {
+                       int lo_a_smem, int lo_b_smem, int tma_c, const GatherGeom gg) {
   constexpr int TC_STAGES = TcStages<BN>::n;  // shadows the default ring depth
   constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4, B_BYTES = BN * TC_BK * 4;
   constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
@@ -175,7 +185,9 @@ __global__ void __launch_bounds__(320, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      // GATHER: the producer lane's expect_tx + one cp.async completion
+      // arrival per producer lane
+      mbar_init(&full[s], GATHER ? 33 : 1);
       mbar_init(&empty[s], 1);
       mbar_init(&conv[s], 4);
     }
@@ -198,7 +210,73 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tmem = *tmem_slot;
   const int nk_all = (K + TC_BK - 1) / TC_BK;
 
-  if (warp == 0) {
+  if (GATHER && warp == 0) {
+    // all 32 lanes gather A (lane l: 16-byte chunk l % 8 of rows l / 8 + 4 i);
+    // lane 0 also loads B with the TMA
+    uint32_t g = 0;
+    const int j = lane & 7;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int z = t / tiles_mn, mn = t - z * tiles_mn;
+      const int m0 = (mn / tiles_n) * TC_BM, n0 = (mn % tiles_n) * BN;
+      const int kb0 = z * kb_per_split;
+      const int kb1 = kb0 + kb_per_split < nk_all ? kb0 + kb_per_split : nk_all;
+      int base[32], hw[32];  // pixel index of tap (0, 0); (ih0 << 16) | (iw0 & 0xffff)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int m = m0 + (lane >> 3) + 4 * i;
+        if (m < M) {
+          const int n = m / gg.howo, rem = m - n * gg.howo;
+          const int oh = rem / gg.wo, ow = rem - oh * gg.wo;
+          const int ih0 = oh * gg.s - gg.p, iw0 = ow * gg.s - gg.p;
+          base[i] = (n * gg.h + ih0) * gg.w + iw0;
+          hw[i] = (ih0 << 16) | (iw0 & 0xffff);
+        } else {
+          base[i] = 0;
+          hw[i] = (int)(0x80000000u);  // ih0 = -32768: never inside the image
+        }
+      }
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        const int s = g % TC_STAGES;
+        if (g >= TC_STAGES) mbar_wait(&empty[s], ((g / TC_STAGES) & 1u) ^ 1u);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        const int kx = kb * TC_BK;
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], lo_b_smem ? B_BYTES : 2 * B_BYTES);
+          if constexpr (BMN) {
+#pragma unroll
+            for (int jj = 0; jj < BN / 32; ++jj) {
+              tma_load_2d(st + 2 * A_BYTES + 4096 * jj, &tBhi, &full[s], n0 + 32 * jj, kx);
+              if (!lo_b_smem)
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES + 4096 * jj, &tBlo, &full[s],
+                            n0 + 32 * jj, kx);
+            }
+          } else {
+            tma_load_2d(st + 2 * A_BYTES, &tBhi, &full[s], kx, n0);
+            if (!lo_b_smem) tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tBlo, &full[s], kx, n0);
+          }
+        }
+        const int tap = kx / gg.c, c0 = kx - tap * gg.c;
+        const int kh = tap / gg.kw, kw = tap - kh * gg.kw;
+        const float* xs = gg.x + c0 + 4 * j;
+        const int off = kh * gg.w + kw;
+        const uint32_t sa = smem_u32(st);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int r = (lane >> 3) + 4 * i;
+          const int ih = (hw[i] >> 16) + kh, iw = (int)(short)(hw[i] & 0xffff) + kw;
+          const bool ok = (unsigned)ih < (unsigned)gg.h && (unsigned)iw < (unsigned)gg.w;
+          const float* src = ok ? xs + (long long)(base[i] + off) * gg.c : gg.x;
+          const uint32_t dst = sa + (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                       "r"(ok ? 16 : 0)
+                       : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         smem_u32(&full[s]))
+                     : "memory");
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       uint32_t g = 0;  // k-blocks issued so far (all tiles): ring position
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -263,6 +341,12 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t b_hi = base + 2 * A_BYTES, b_lo = base + 2 * A_BYTES + B_BYTES;
           const uint32_t pa[3] = {a_hi, a_hi, a_lo};
           const uint32_t pb[3] = {b_hi, b_lo, b_hi};
+          if (GATHER) {
+            // the A tile came through cp.async (generic proxy; its completion
+            // is observed through the full barrier): order it before this
+            // thread's async-proxy (tensor core) reads
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          }
 #pragma unroll
           for (int pass = 0; pass < 3; ++pass) {
             if (pass == 1 && any_lo) {
@@ -597,16 +681,24 @@ static bool no_tma_store() {
 // ak / bk: the contraction extent each operand actually stores (<= K; the
 // TMA boxes zero-fill beyond it).  K-major: the row length (leading
 // dimension); MN-major: the number of rows.
-template <int BN, bool AMN, bool BMN>
+template <int BN, bool AMN, bool BMN, bool GATHER = false>
 static int run_tc(Device* d, long long M, long long N, long long K, long long ak, long long bk,
                   const float* ahi, const float* alo, const float* bhi, const float* blo,
-                  float* c) {
+                  float* c, const GatherGeom* gat = nullptr) {
   // a null lo pointer: that operand's lo part is derived in shared memory
   const int lo_a_smem = alo == nullptr, lo_b_smem = blo == nullptr;
   if (lo_a_smem) alo = ahi;  // the (unused) lo map still needs a valid encoding
   if (lo_b_smem) blo = bhi;
   CUtensorMap ta, tal, tb, tbl;
-  if (AMN) {
+  if (GATHER) {
+    // A is gathered by the producer warp; its maps are unused (any valid map)
+    if (BMN) {
+      SF_TRY(encode_map(&ta, bhi, bk, N, 32, true));
+    } else {
+      SF_TRY(encode_map(&ta, bhi, N, bk, BN));
+    }
+    tal = ta;
+  } else if (AMN) {
     SF_TRY(encode_map(&ta, ahi, ak, M, 32, true));
     SF_TRY(encode_map(&tal, alo, ak, M, 32, true));
   } else {
@@ -625,7 +717,7 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
                    4 * 8192;
   static bool configured[64] = {};
   if (!configured[d->id]) {
-    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN, AMN, BMN>,
+    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_persistent<BN, AMN, BMN, GATHER>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured[d->id] = true;
   }
@@ -661,9 +753,11 @@ static int run_tc(Device* d, long long M, long long N, long long K, long long ak
   } else {
     tc = ta;  // unused
   }
-  gemm_tc_persistent<BN, AMN, BMN><<<grid, 320, smem, d->stream>>>(
+  GatherGeom gg{};
+  if (gat) gg = *gat;
+  gemm_tc_persistent<BN, AMN, BMN, GATHER><<<grid, 320, smem, d->stream>>>(
       ta, tal, tb, tbl, tc, out, (int)M, (int)N, (int)K, (int)per, (int)tiles_n, (int)tiles,
-      (int)n_tiles, lo_a_smem, lo_b_smem, tma_c);
+      (int)n_tiles, GATHER ? 1 : lo_a_smem, lo_b_smem, tma_c, gg);
   if (splits == 1) {
     count_launch(d->id);
     SF_CHECK_CUDA(cudaGetLastError());
@@ -712,9 +806,39 @@ int launch_gemm_tc_ex(Device* d, int64_t M, int64_t N, int64_t K, bool amn, bool
     return e ? atoi(e) : 1;
   }();
   const long long tiles256 = ((N + 255) / 256) * ((M + TC_BM - 1) / TC_BM);
-  if (bn256 && N >= 256 && tiles256 >= d->sm_count)
+  // (bn256 >= 2: also for long contractions, where split-K fills the SMs)
+  const bool long_k = (K + TC_BK - 1) / TC_BK >= 64;
+  if (bn256 && N >= 256 && (tiles256 >= d->sm_count || (bn256 >= 2 && long_k)))
     return run_tc_major<256>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
   return run_tc_major<128>(d, M, N, K, amn, bmn, ak, bk, ahi, alo, bhi, blo, c);
+}
+
+// Implicit-GEMM convolution: out[N*HO*WO, co] = im2col(x) . W, W (kh*kw*c, co)
+// row-major read MN-major; x NHWC with c % 32 == 0 (one filter tap per
+// 32-wide k-block).  Same tiles, passes and k order as the explicit
+// im2col + GEMM path, so the result is bit-identical to it.
+int launch_conv_tc(Device* d, const int64_t* g8, int64_t co, const float* x, const float* w,
+                   float* out) {
+  const long long n = g8[0], h = g8[1], wd = g8[2], c = g8[3], kh = g8[4], kw = g8[5];
+  const long long st = g8[6], pd = g8[7];
+  const long long ho = (h + 2 * pd - kh) / st + 1, wo = (wd + 2 * pd - kw) / st + 1;
+  const long long M = n * ho * wo, K = kh * kw * c;
+  if (c % 32 != 0 || co % 4 != 0 || (uintptr_t)x % 16 != 0 || n * h * wd >= (1ll << 31) ||
+      M >= (1ll << 31) || h >= 32768 || wd >= 32768 || pd >= 16384) {
+    set_error("conv_tc: needs C % 32 == 0, Cout % 4 == 0, a 16-byte aligned input and "
+              "32-bit pixel indices");
+    return SF_ERR_INVALID;
+  }
+  if (M == 0 || co == 0) return SF_OK;
+  GatherGeom gg{x, (int)h, (int)wd, (int)c, (int)kw, (int)st, (int)pd, (int)wo, (int)(ho * wo)};
+  if (co <= 64) return run_tc<64, false, true, true>(d, M, co, K, K, K, nullptr, nullptr, w,
+                                                     nullptr, out, &gg);
+  const long long tiles256 = ((co + 255) / 256) * ((M + TC_BM - 1) / TC_BM);
+  if (co >= 256 && tiles256 >= d->sm_count)
+    return run_tc<256, false, true, true>(d, M, co, K, K, K, nullptr, nullptr, w, nullptr, out,
+                                          &gg);
+  return run_tc<128, false, true, true>(d, M, co, K, K, K, nullptr, nullptr, w, nullptr, out,
+                                        &gg);
 }
 
 int launch_gemm_tc(Device* d, int64_t M, int64_t N, int64_t K, const float* ahi, const float* alo,
@@ -774,6 +898,16 @@ int sf_gemm_tf32x3_ex(int dev, int64_t m, int64_t n, int64_t k, int a_mn, int b_
   return launch_gemm_tc_ex(d, m, n, k, a_mn != 0, b_mn != 0, ak, bk, (const float*)a_hi,
                            (const float*)a_lo, (const float*)b_hi, (const float*)b_lo,
                            (float*)*c);
+}
+
+int sf_conv2d_tc(int dev, const int64_t* g8, int64_t co, const void* x, const void* w,
+                 void** out) {
+  Device* d;
+  SF_TRY(ensure_device(dev, &d));
+  const long long ho = (g8[1] + 2 * g8[7] - g8[4]) / g8[6] + 1;
+  const long long wo = (g8[2] + 2 * g8[7] - g8[5]) / g8[6] + 1;
+  if (*out == nullptr) SF_TRY(d->alloc.alloc(dev, (size_t)(g8[0] * ho * wo * co) * 4, out));
+  return launch_conv_tc(d, g8, co, (const float*)x, (const float*)w, (float*)*out);
 }
 
 int sf_split_tf32(int dev, int64_t rows, int64_t cols, int64_t ldo, int transpose, const void* x,

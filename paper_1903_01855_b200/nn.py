@@ -49,6 +49,10 @@ def _ceil4(v: int) -> int:
 # part in shared memory from the tile it loaded (sf_gemm_tc.cu converter
 # warps).  False: lo parts are precomputed by a separate split pass.
 LO_IN_SMEM = True
+# float32 convolutions with C % 32 == 0 as implicit GEMMs (sf_conv2d_tc: no
+# materialised im2col matrix); bit-identical to the explicit path
+IMPLICIT_CONV = __import__("os").environ.get("SF_IMPLICIT_CONV", "1") == "1"
+IMPLICIT_MAX_K = int(__import__("os").environ.get("SF_IMPLICIT_MAX_K", "1152"))
 
 
 def _lo(pair) -> int:
@@ -112,7 +116,17 @@ def _conv_kernel(attrs, inputs, env):
     ho, wo = _out_hw(h, wd, kh, s, p)
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
-    if _use_tc(x.dtype):
+    if _use_tc(x.dtype) and IMPLICIT_CONV and c % 32 == 0 and co % 4 == 0 and \
+            not _is_pointwise(kh, kw, s, p) and s == 1 and k <= IMPLICIT_MAX_K:
+        # implicit GEMM: the im2col rows are gathered by the GEMM itself
+        # (B200, ResNet-50 b32 forward: layer1 3x3 167 -> 141 us, layer2
+        # 109 -> 92 us; slower where the 16-byte cp.async gathers of long
+        # contractions / strided windows replace one TMA box: layer3 80 ->
+        # 87 us, layer4 79 -> 103 us, 1x1 stride 2 54 -> 65 us —
+        # tools/conv_time.py)
+        out = _native.nn_call("sf_conv2d_tc", dev, _geom(n, h, wd, c, kh, kw, s, p), co,
+                              x._ptr(), w._ptr(), out_nbytes=m * co * 4)
+    elif _use_tc(x.dtype):
         kp = _ceil4(k)
         if _is_pointwise(kh, kw, s, p) and kp == k:
             a = _raw(dev, m, k, x._ptr())  # x itself is the A operand

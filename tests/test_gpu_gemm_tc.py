@@ -113,3 +113,37 @@ def test_gemm_lo_in_shared_memory_bitwise(a_mn, b_mn, lo_a, lo_b, m, n, k, ak, b
                                  0 if lo_a else al.ptr, tb._ptr(), 0 if lo_b else bl.ptr)
     r = _native.download(ref, np.float32, (m, n))
     assert _native.download(got, np.float32, (m, n)).tobytes() == r.tobytes()
+
+
+@pytest.mark.parametrize("shape,filt,s,p", [
+    ((2, 14, 14, 64), (3, 3, 64, 64), 1, 1),       # layer1-like 3x3, partial last tile
+    ((3, 9, 11, 32), (3, 3, 32, 96), 1, 1),        # odd spatial extents, BN=128 path
+    ((2, 16, 16, 128), (3, 3, 128, 128), 2, 1),    # strided 3x3 (layer2 entry)
+    ((2, 14, 14, 256), (1, 1, 256, 512), 2, 0),    # strided 1x1 downsample
+    ((2, 15, 15, 64), (5, 5, 64, 32), 3, 2),       # other window / stride / pad
+    ((4, 28, 28, 64), (3, 3, 64, 256), 1, 1),      # BN=256 tiles
+    ((1, 7, 7, 512), (3, 3, 512, 512), 1, 1),      # late layer: K = 4608, few tiles
+])
+def test_implicit_conv_equals_explicit_im2col_gemm(shape, filt, s, p, monkeypatch):
+    """sf_conv2d_tc (the GEMM gathers its im2col rows with cp.async) is
+    bit-identical to the explicit im2col + GEMM path, and fp32-accurate
+    against a float64 convolution."""
+    from paper_1903_01855_b200 import nn
+    from oracle import nn_np
+
+    nn.install()
+    rng = np.random.default_rng(sum(shape) + sum(filt))
+    x = rng.standard_normal(shape).astype(np.float32)
+    w = (rng.standard_normal(filt) / np.sqrt(filt[0] * filt[1] * filt[2])).astype(np.float32)
+    tx, tw = sf.constant(x), sf.constant(w)
+    monkeypatch.setattr(nn, "IMPLICIT_CONV", True)
+    monkeypatch.setattr(nn, "IMPLICIT_MAX_K", 1 << 30)
+    launches0 = _native.launch_count(0)
+    got = nn.conv2d(tx, tw, stride=s, pad=p).numpy()
+    implicit_launches = _native.launch_count(0) - launches0
+    monkeypatch.setattr(nn, "IMPLICIT_CONV", False)
+    ref = nn.conv2d(tx, tw, stride=s, pad=p).numpy()
+    np.testing.assert_array_equal(got, ref)
+    assert implicit_launches <= 2  # the GEMM (+ a split-K reduce), no im2col kernel
+    want = nn_np.conv2d(x.astype(np.float64), w.astype(np.float64), s, p)
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4)
