@@ -288,6 +288,17 @@ SF_DEVFN void cp_async(void* smem, const void* gmem) {
                : "memory");
 }
 SF_DEVFN void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// One G-byte chunk of a staged operand (elements of W bytes), copied with
+// cp.async: a single 16-byte copy when the source is 16-byte aligned.
+template <int G, int W>
+SF_DEVFN void stage_chunk(unsigned char* dst, const unsigned char* src) {
+  if (G == 16 && (((unsigned long long)src) & 15) == 0) {
+    cp_async<16>(dst, src);
+  } else {
+#pragma unroll
+    for (int e = 0; e < G / W; ++e) cp_async<W>(dst + W * e, src + W * e);
+  }
+}
 
 // Volatile shared-memory reads of staged uniform operands.  A row program
 // reads the same weights once per network evaluation; plain loads let ptxas

@@ -715,6 +715,100 @@ def find_teams(rp: RowProgram, planner) -> Optional[Tuple[List[LOp], List[LOp], 
             xfer[0], xfer[1])
 
 
+# re-roll runs of identical uniform-kernel levels (see _uniform_prologue)
+UNI_REROLL = __import__("os").environ.get("SF_UNI_REROLL", "1") == "1"
+UNI_REROLL_MIN = 3
+# extra warps of a uniform kernel that only help stage its operands (C2: 1 -> 4
+# warps, 24.7 -> 19.6 us per chain; 8: no further gain)
+UNI_MIN_WARPS = int(__import__("os").environ.get("SF_UNI_MIN_WARPS", "4"))
+_UNI_TOK = re.compile(r"\bU(\d+)\b|\bdsm \+ (\d+)\b|\ba\.p\[(\d+)\]")
+
+
+def _stage_loops(loads: List[Tuple[int, int, int, int]]) -> List[str]:
+    """cp.async staging of a uniform kernel's global operands: operands of
+    one size whose pointer slots and shared offsets advance by fixed strides
+    (a traced loop's per-layer weights) are staged by one loop over the slots
+    (each line contains "int q": it is a load, see _generate)."""
+    by_class: Dict[Tuple[int, int], List[Tuple[int, int]]] = {}
+    for k, off, nb, w in loads:
+        by_class.setdefault((nb, w), []).append((k, off))
+    out = []
+    for (nb, w), items in by_class.items():
+        i = 0
+        while i < len(items):
+            m = 1
+            if i + 1 < len(items):
+                dk = items[i + 1][0] - items[i][0]
+                do = items[i + 1][1] - items[i][1]
+                while (i + m < len(items) and items[i + m][0] == items[i][0] + dk * m
+                       and items[i + m][1] == items[i][1] + do * m):
+                    m += 1
+            k0, o0 = items[i]
+            if m < 3:
+                m, dk, do = 1, 0, 0
+            # one flattened loop over (operand, 16-byte chunk): independent
+            # iterations, so the CTA keeps many copies in flight
+            g = 16 if nb % 16 == 0 else w
+            ch = nb // g
+            out.append(f"  for (int q = threadIdx.x; q < {m * ch}; q += blockDim.x) {{ "
+                       f"const int t = q / {ch}, c = q - t * {ch}; "
+                       f"sf::stage_chunk<{g}, {w}>(dsm + {o0} + {do} * t + {g} * c, "
+                       f"(const unsigned char*)a.p[{k0} + {dk} * t] + {g} * c); }}")
+            i += m
+    return out
+
+
+def _uni_canon(code: str, offs) -> Tuple[str, List[int]]:
+    """(template, values): the uniform pool arrays U<id>, staged-operand
+    offsets `dsm + N` and pointer slots `a.p[k]` of a level's code replaced by
+    numbered holes; values[k] fills hole k (U arrays become pool byte
+    offsets, tagged by element type in the template)."""
+    vals: List[int] = []
+    out = []
+    last = 0
+    for mt in _UNI_TOK.finditer(code):
+        out.append(code[last:mt.start()])
+        k = len(vals)
+        if mt.group(1) is not None:
+            off, ct = offs[int(mt.group(1))]
+            vals.append(off)
+            out.append(f"(({ct}*)(upool + @{k}@))")
+        elif mt.group(2) is not None:
+            vals.append(int(mt.group(2)))
+            out.append(f"dsm + @{k}@")
+        else:
+            vals.append(int(mt.group(3)))
+            out.append(f"a.p[@P{k}@]")
+        last = mt.end()
+    out.append(code[last:])
+    return "".join(out), vals
+
+
+def _uni_arith(canon, i: int, m: int) -> bool:
+    """Levels i .. i+m-1: every hole's value advances by a fixed stride
+    (pointer slots must stay fixed: the parameter array is not indexed at
+    run time)."""
+    t0 = canon[i][0]
+    v0, v1 = canon[i][1], canon[i + 1][1]
+    if len(v0) != len(v1):
+        return False
+    d = [b - a for a, b in zip(v0, v1)]
+    for k in range(len(v0)):
+        if f"@P{k}@" in t0 and d[k] != 0:
+            return False
+    for q in range(m):
+        vq = canon[i + q][1]
+        if len(vq) != len(v0) or any(vq[k] != v0[k] + d[k] * q for k in range(len(v0))):
+            return False
+    return True
+
+
+def _uni_fill(text: str, vals: List[str]) -> str:
+    for k in range(len(vals) - 1, -1, -1):
+        text = text.replace(f"@P{k}@", vals[k]).replace(f"@{k}@", vals[k])
+    return text
+
+
 def _uniform_smem(rp: RowProgram) -> int:
     """Shared memory a uniform kernel needs for its computed values."""
     return sum(o.nbytes for op in rp.ops for o in op.outs)
@@ -774,10 +868,13 @@ class _Gen:
         self.staged: Dict[int, str] = {}
         self.uni_smem = _uniform_smem(rp) if rp.uniform_only else 0
         self.dyn = 0  # dynamic shared memory of the uniform kernel (staged operands)
+        self.dyn_loads: List[Tuple[int, int, int, int]] = []  # (slot, dsm offset, bytes, width)
         self.cse: Dict[tuple, LV] = {}
         self.alias: Dict[int, LV] = {}
         self.level: Dict[int, int] = {}
         self.uni_ops: List[Tuple[int, int, str, tuple]] = []  # (level, work, code, out shape)
+        self.upool: List[Tuple[int, str, int, int]] = []  # (U id, ctype, elements, width)
+        self.upool_offs: Dict[int, Tuple[int, str]] = {}
         self.uni_entry: Dict[int, int] = {}  # uniform op output id -> its uni_ops entry
         self.block = 128
         self.f2vars: set = set()  # names declared float2 (packed row pairs)
@@ -876,10 +973,7 @@ class _Gen:
             if width in (4, 8) and off + n * width <= budget:
                 self.dyn = off + n * width
                 self.staged[id(r)] = f"((const {ct}*)(dsm + {off}))"
-                self.smem.append(
-                    f"  for (int q = threadIdx.x; q < {n}; q += blockDim.x) "
-                    f"sf::cp_async<{width}>(dsm + {off} + {width} * q, "
-                    f"&((const {ct}*)a.p[{k}])[q]);")
+                self.dyn_loads.append((k, off, n * width, width))
         else:
             self.ext_kind.append(UNI)
             pidx, _ = self._stage(r, f"s{k}", [k])
@@ -1086,7 +1180,9 @@ class _Gen:
                     fold = e
                     level -= 1
         self.level[id(o)] = level
-        self.smem.append(f"  __shared__ __align__(16) {ct} U{o.id}[{max(1, n)}];")
+        # computed uniform values live in one shared pool (placed by
+        # _uniform_prologue), so re-rolled levels can address them by iteration
+        self.upool.append((o.id, ct, max(1, n), o.dtype.width))
         self.uni_names[id(o)] = [f"U{o.id}[{q}]" for q in range(n)]
         k = op.kind
         shape = o.shape
@@ -1154,28 +1250,73 @@ class _Gen:
         self.uni_ops.append((level, work, loop + body + " }", shape))
 
     def _uniform_prologue(self) -> None:
-        """Level-by-level schedule of the uniform ops over up to 32 warps."""
+        """Level-by-level schedule of the uniform ops over up to 32 warps.
+
+        Computed values sit in one shared pool (`upool`).  Runs of at least
+        UNI_REROLL_MIN consecutive levels whose code is identical up to pool
+        offsets and staged-operand offsets that advance by a fixed stride (a
+        traced loop's layers: C2's 100 x tanh(x W_i + b_i)) are emitted as
+        one loop over the level index: each iteration executes exactly the
+        straight-line level's statements at the same addresses, so results
+        are unchanged, while the kernel's code shrinks ~m-fold (the
+        straight-line C2 kernel was instruction-fetch bound: one warp
+        walking ~100 KB of SASS once per call)."""
+        self.smem += _stage_loops(self.dyn_loads)
         if not self.uni_ops:
             return
+        offs: Dict[int, Tuple[int, str]] = {}
+        pos = 0
+        for uid, ct, n, width in self.upool:
+            pos = -(-pos // 16) * 16
+            offs[uid] = (pos, ct)
+            pos += n * width
+        if pos:
+            self.smem.append(f"  __shared__ __align__(16) unsigned char upool[{pos}];")
+        self.upool_offs = offs
         levels: Dict[int, List[Tuple[int, str]]] = {}
         for level, work, code, _shape in self.uni_ops:
             levels.setdefault(level, []).append((work, code))
         warps = max(1, min(32, max(len(v) for v in levels.values())))
-        self.block = 32 * warps
-        out = ["  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;"]
-        for i, level in enumerate(sorted(levels)):
+        # extra warps only stage operands (more cp.async in flight)
+        nw = max(warps, UNI_MIN_WARPS if self.dyn_loads else 1)
+        self.block = 32 * nw
+        blocks = []
+        for level in sorted(levels):
             load = [0] * warps
             assign: List[List[str]] = [[] for _ in range(warps)]
             for work, code in sorted(levels[level], key=lambda wc: -wc[0]):
                 w = load.index(min(load))
                 load[w] += work + 32
                 assign[w].append(code)
+            parts = []
             for w, codes in enumerate(assign):
                 if codes:
-                    cond = "" if warps == 1 else f"if (warp == {w}) "
-                    out.append(f"  {cond}{{\n  " + "\n  ".join(codes) + "\n  }")
-            if i + 1 < len(levels):
-                out.append("  __syncthreads();")
+                    cond = "" if nw == 1 else f"if (warp == {w}) "
+                    parts.append(f"  {cond}{{\n  " + "\n  ".join(codes) + "\n  }")
+            blocks.append("\n".join(parts))
+        canon = [_uni_canon(b, offs) for b in blocks]
+        out = ["  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;"]
+        i = 0
+        while i < len(blocks):
+            m = 1
+            while (i + m < len(blocks) and canon[i + m][0] == canon[i][0]
+                   and _uni_arith(canon, i, m + 1)):
+                m += 1
+            last = i + m == len(blocks)
+            if UNI_REROLL and m >= UNI_REROLL_MIN:
+                text, vals = canon[i]
+                d = [b - a for a, b in zip(vals, canon[i + 1][1])]
+                body = _uni_fill(text, [f"({v} + {dv} * it)" if dv else str(v)
+                                        for v, dv in zip(vals, d)])
+                out.append(f"#pragma unroll 1\n  for (int it = 0; it < {m}; ++it) {{\n{body}"
+                           "\n  __syncthreads();\n  }")
+            else:
+                for q in range(i, i + m):
+                    out.append(_uni_fill(canon[q][0], [str(v) for v in canon[q][1]]))
+                    if q + 1 < len(blocks):
+                        out.append("  __syncthreads();")
+            i += m
+            del last
         self.prologue = out
 
     def row_elem(self, x: LV, j: int, out_w: int, out_rank: int) -> str:
@@ -1732,6 +1873,9 @@ def _generate(rp: RowProgram, planner: RowPlanner, needed: set):
     if g.prologue:
         src.append("  __syncthreads();")
     if uni_stores:
+        if g.upool_offs:
+            uni_stores = [_uni_fill(t, [str(v) for v in vs])
+                          for t, vs in (_uni_canon(x, g.upool_offs) for x in uni_stores)]
         src.append("  if (blockIdx.x == 0) {\n    " + "\n    ".join(uni_stores) + "\n  }")
     if rp.uniform_only:
         src.append("}\n")

@@ -66,7 +66,13 @@ def main():
     os.makedirs(out, exist_ok=True)
     sf.init_runtime(sf.RuntimeOptions())
     plugins.install()
-    if "--leapfrog" in sys.argv:
+    if "--c2" in sys.argv:
+        from paper_1903_01855_b200.workloads import microbench
+
+        ch = microbench.Chain("staged")
+        pf = ch.fn
+        args = [ch.x]
+    elif "--leapfrog" in sys.argv:
         from paper_1903_01855_b200.workloads.leapfrog import Leapfrog
 
         wl = Leapfrog(batch, "staged")
