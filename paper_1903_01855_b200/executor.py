@@ -27,7 +27,7 @@ from .errors import (CallbackError, DeadVariable, InputMismatch, KernelError, Mi
 from .graph import GraphFunction, Node
 from .kernels import KernelEnv, ordinal_of, relabel
 from .lowering import (FusedGroup, LOp, Lowerer, LV, PlanWriter, SLOT_CONST, SLOT_INPUT,
-                       alias_unwritten_reads,
+                       alias_unwritten_reads, elide_zero_adds,
                        SLOT_OUTPUT, SLOT_TEMP, cse, fuse, fuse_reductions, generate_group,
                        generate_reduce_group, pack_ew_step)
 from .runtime import current_context, get_runtime
@@ -153,6 +153,8 @@ class Program:
         keep = frozenset(id(v.root()) for v in self.out_vals)
         ops = alias_unwritten_reads(lw.ops, keep) if fuse_enabled else lw.ops
         ops = cse(ops) if fuse_enabled else ops
+        if fuse_enabled and ELIDE_ZERO_ADDS:
+            ops = elide_zero_adds(ops, keep)
         self.has_rng = any(op.kind in ("rng", "dropout") for op in ops)
         keep = frozenset(id(v.root()) for v in self.out_vals)
         units = fuse(plan_rows(ops, keep) if fuse_enabled else ops, fuse_enabled)
@@ -691,6 +693,8 @@ class Program:
 # the identity of those tensors (tensors are immutable; a capture of a trace
 # is the same object on every call).  SF_BAKE=0 disables it.
 BAKE = __import__("os").environ.get("SF_BAKE", "1") == "1"
+# drop x + (+0) whose result only reaches relu (lowering.elide_zero_adds)
+ELIDE_ZERO_ADDS = __import__("os").environ.get("SF_ELIDE_ZERO_ADDS", "1") == "1"
 BAKE_MAX_NUMEL = 1024
 # tensors captured by a ConcreteFunction (staging.py): the same immutable
 # object is passed on every call of that function

@@ -336,6 +336,76 @@ class FusedGroup:
 _PURE_KINDS = frozenset(("ew", "matmul", "reduce", "transpose", "eye"))
 
 
+def _is_pos_zero(v: LV) -> bool:
+    """v is a float constant (splat literal or specialised capture) whose
+    every element is +0.0."""
+    r = v.root()
+    if not r.dtype.is_float:
+        return False
+    if r.kind == "const" and r.imm is not None:
+        return float(r.imm) == 0.0 and not np.signbit(r.imm)
+    if r.vals is not None:
+        a = np.asarray(r.vals)
+        return a.size > 0 and not a.any() and not np.signbit(a).any()
+    return False
+
+
+def elide_zero_adds(ops: List[LOp], keep) -> List[LOp]:
+    """x + (+0) -> x where the sum only reaches relu through add/sub chains.
+
+    x + (+0) equals x except that -0 becomes +0.  Two values that differ only
+    in the sign of a zero still differ only that way after adding or
+    subtracting any third value, and relu maps both zeros to +0 (NaNs pass
+    unchanged), so every relu output is bit-identical with the add removed.
+    A network layer with zero-initialised biases (the L2HMC nets) thereby
+    drops one vector add per layer.  Values the program returns (keep) and
+    any other consumer keep the add."""
+    users: Dict[int, List[LOp]] = {}
+    for op in ops:
+        for x in op.ins:
+            users.setdefault(id(x.root()), []).append(op)
+    memo: Dict[int, bool] = {}
+
+    def insensitive(v: LV, depth: int = 0) -> bool:
+        r = v.root()
+        if id(r) in memo:
+            return memo[id(r)]
+        ok = id(r) not in keep and depth < 16 and bool(users.get(id(r)))
+        if ok:
+            for u in users[id(r)]:
+                if u.kind != "ew" or len(u.outs) != 1:
+                    ok = False
+                elif u.name == "relu":
+                    continue
+                elif u.name in ("add", "sub") and u.outs[0].shape == v.shape:
+                    if not insensitive(u.outs[0], depth + 1):
+                        ok = False
+                else:
+                    ok = False
+                if not ok:
+                    break
+        memo[id(r)] = ok
+        return ok
+
+    out: List[LOp] = []
+    for op in ops:
+        if (op.kind == "ew" and op.name == "add" and len(op.ins) == 2 and len(op.outs) == 1
+                and op.outs[0].dtype.is_float):
+            o = op.outs[0]
+            for a, b in ((op.ins[0], op.ins[1]), (op.ins[1], op.ins[0])):
+                if (_is_pos_zero(b) and tuple(a.shape) == tuple(o.shape)
+                        and a.dtype is o.dtype and insensitive(o)):
+                    o.kind = "alias"
+                    o.base = a
+                    o.producer = None
+                    break
+            else:
+                out.append(op)
+            continue
+        out.append(op)
+    return out
+
+
 def cse(ops: List[LOp]) -> List[LOp]:
     """Common-subexpression elimination over deterministic ops.
 

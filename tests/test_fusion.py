@@ -139,3 +139,30 @@ def test_variable_update_folds_into_increment_group_unless_touched():
     assert [op.name for op in groups[0].ops] == ["mul", "add", "mul"]
     # w's update: w was read after the group ran, so it stays a separate op
     assert any(isinstance(u, LOp) and u.kind == "var_add" for u in units)
+
+
+def test_zero_bias_add_elided_only_before_relu():
+    """x + (+0) is dropped when its value reaches only relu through add/sub
+    (sign-of-zero differences vanish there); a -0 bias, a kept value, or a
+    multiply on the way keeps the add."""
+    import numpy as np
+
+    def net(bias_vals, tail="relu", keep_sum=False):
+        P = _Prog()
+        x = P.lv((4, 10), "input")
+        t = P.lv((4, 10), "input")
+        b = P.lv((10,), "input")
+        b.vals = np.asarray(bias_vals, np.float32)
+        z = P.op("ew", "add", [x, b], (4, 10))
+        s = P.op("ew", "add", [t, z], (4, 10))
+        y = P.op("ew", tail, [s, s] if tail == "mul" else [s], (4, 10))
+        keep = {id(y)} | ({id(s)} if keep_sum else set())
+        return P, x, z, lowering.elide_zero_adds(P.ops, frozenset(keep))
+
+    P, x, z, ops = net(np.zeros(10))
+    assert [op.name for op in ops] == ["add", "relu"] and z.root() is x
+    for kwargs in ({"bias_vals": -np.zeros(10)}, {"bias_vals": np.r_[np.zeros(9), 1.0]},
+                   {"bias_vals": np.zeros(10), "tail": "mul"},
+                   {"bias_vals": np.zeros(10), "keep_sum": True}):
+        P, x, z, ops = net(**kwargs)
+        assert len(ops) == 3 and z.root() is z, kwargs

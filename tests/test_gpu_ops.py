@@ -269,3 +269,22 @@ def test_random_programs_eager_equals_staged(seed):
     staged = sf.stage(fn)(*inputs)
     assert eager.dtype is staged.dtype and eager.shape == staged.shape
     assert eager.raw().tobytes() == staged.raw().tobytes(), seed
+
+
+def test_zero_bias_elision_is_bitwise_with_signed_zeros():
+    """A staged relu(t + (x + 0-bias)) with +-0 / NaN / inf inputs: the add
+    the staged compiler drops (lowering.elide_zero_adds) changes no bit of
+    the relu output against the eager path, which performs it."""
+    vals = np.array([0.0, -0.0, 1.0, -1.0, np.nan, np.inf, -np.inf, 1e-45, -1e-45, 3.0],
+                    np.float32)
+    x = np.stack([vals, vals[::-1], -vals, np.roll(vals, 3)]).astype(np.float32)
+    t = np.stack([-vals, vals, np.roll(vals, 5), vals[::-1]]).astype(np.float32)
+    bias = sf.constant(np.zeros(10, np.float32))
+
+    def f(a, b):
+        return sf.relu(sf.add(b, sf.add(a, bias)))
+
+    tx, tt = sf.constant(x), sf.constant(t)
+    eager = f(tx, tt).numpy()
+    staged = sf.stage(f)(tx, tt).numpy()
+    np.testing.assert_array_equal(eager.view(np.uint32), staged.view(np.uint32))

@@ -97,8 +97,11 @@ def main():
             lv.tensor = v
         ins.append(lv)
     outs = lw.lower_graph(gf, ins, ())
-    ops = cse(lw.ops)
     keep = frozenset(id(v.root()) for v in outs)
+    ops = cse(lw.ops)
+    if executor.ELIDE_ZERO_ADDS:
+        from paper_1903_01855_b200.lowering import elide_zero_adds
+        ops = elide_zero_adds(ops, keep)
     units = rowfuse.plan_rows(ops, keep)
     k = 0
     shutil.copy(os.path.join(ROOT, "paper_1903_01855_b200", "csrc", "sf_ops.cuh"), out)
