@@ -119,6 +119,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 // tf32 split of 4 values: *h = x with the low 13 mantissa bits cleared
 // (what the tensor core reads of x), returns lo = x - hi (exact in fp32)
 __device__ __forceinline__ float4 tf32_lo4(float4 v, float4* h) {
@@ -383,22 +398,27 @@ __global__ void __launch_bounds__(320, 1)
           const int s = g % TC_STAGES;
           mbar_wait(&full[s], (g / TC_STAGES) & 1u);
           uint8_t* st = smem + s * STAGE_BYTES;
+          // shared-window addressing (ld/st.shared, not generic LD/ST)
           if (lo_a_smem) {
-            const float4* hi = reinterpret_cast<const float4*>(st);
-            float4* lo = reinterpret_cast<float4*>(st + A_BYTES);
+            const uint32_t hi = smem_u32(st), lo = hi + A_BYTES;
+            float4 v[A_BYTES / 16 / 128];
+#pragma unroll
+            for (int i = 0; i < (int)(A_BYTES / 16 / 128); ++i) v[i] = lds128(hi + (ct + 128 * i) * 16);
 #pragma unroll
             for (int i = 0; i < (int)(A_BYTES / 16 / 128); ++i) {
               float4 h;
-              lo[ct + 128 * i] = tf32_lo4(hi[ct + 128 * i], &h);
+              sts128(lo + (ct + 128 * i) * 16, tf32_lo4(v[i], &h));
             }
           }
           if (lo_b_smem) {
-            const float4* hi = reinterpret_cast<const float4*>(st + 2 * A_BYTES);
-            float4* lo = reinterpret_cast<float4*>(st + 2 * A_BYTES + B_BYTES);
+            const uint32_t hi = smem_u32(st + 2 * A_BYTES), lo = hi + B_BYTES;
+            float4 v[B_BYTES / 16 / 128];
+#pragma unroll
+            for (int i = 0; i < (int)(B_BYTES / 16 / 128); ++i) v[i] = lds128(hi + (ct + 128 * i) * 16);
 #pragma unroll
             for (int i = 0; i < (int)(B_BYTES / 16 / 128); ++i) {
               float4 h;
-              lo[ct + 128 * i] = tf32_lo4(hi[ct + 128 * i], &h);
+              sts128(lo + (ct + 128 * i) * 16, tf32_lo4(v[i], &h));
             }
           }
           // generic-proxy smem writes -> visible to the tensor core (async proxy)
