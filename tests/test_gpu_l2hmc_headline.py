@@ -133,3 +133,29 @@ def test_l2hmc_graph_bytes_match_reference(draws):
     gf = pf.cached_functions()[0].graph
     assert serialize(gf) == GOLD2[f"l2hmc_graph_{draws}_200"].tobytes()
     assert pf.trace_count == int(GOLD2[f"l2hmc_graph_{draws}_200_trace_count"][0])
+
+
+@pytest.mark.parametrize("chains,env", [
+    (4737, {}),                                   # just above the balanced-grid threshold
+    (9473, {}),                                   # team-split limit + 1: balanced, no teams
+    (150_001, {}),                                # several CTAs per SM, ragged last CTA
+    (30_011, {"ROW_REPLICAS": 2}),                # two chains per thread (FFMA2 immediates)
+    (30_011, {"LOOP_SYNC": False, "ROW_GRID": "legacy"}),
+])
+def test_row_kernel_geometries_eager_equals_staged_bitwise(chains, env, monkeypatch):
+    """Every row-kernel launch geometry (rowfuse._geometry: balanced grids
+    with partially filled warps, per-iteration CTA barriers, replica rows
+    past a CTA's end, the legacy 128-chain grid) computes each chain exactly
+    as the eager path does."""
+    from paper_1903_01855_b200 import rowfuse
+
+    for k, v in env.items():
+        monkeypatch.setattr(rowfuse, k, v)
+    outs = {}
+    for mode in ("eager", "staged"):
+        sf.init_runtime(sf.RuntimeOptions(seed=77))
+        plugins.install()
+        s = l2hmc.L2HMCSampler(sf, chains, mode, seed=0)
+        outs[mode] = [s.run_iteration() for _ in range(2)]
+    for e, g in zip(outs["eager"], outs["staged"]):
+        assert e.tobytes() == g.tobytes()
