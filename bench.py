@@ -792,8 +792,26 @@ def resnet_extra(sf, np, _native):
     useful = 2.0 * m * n * k / (ms * 1e-3) / 1e12
     tf32 = cpk.get("tcgen05_tf32_tflops")
     peak = tf32 / 3 if tf32 else peaks.get("bf16_tflops", 1590.0) / 6
+    # the same layer as the training step's forward runs it: the implicit-GEMM
+    # convolution (sf_conv2d_tc; the GEMM gathers its im2col rows)
+    from paper_1903_01855_b200 import nn as _nn
+    x4 = sf.constant(np.random.default_rng(2).standard_normal((32, 56, 56, 64)).astype(np.float32))
+    w4 = sf.constant(np.random.default_rng(3).standard_normal((3, 3, 64, 64)).astype(np.float32))
+    for _ in range(3):
+        _nn.conv2d(x4, w4, 1, 1)
+    e0.record(stream)
+    for _ in range(reps):
+        _nn.conv2d(x4, w4, 1, 1)
+    e1.record(stream)
+    _native.sync(0)
+    conv_ms = e0.elapsed_time(e1) / reps
     row["roofline"] = {"kernel": "gemm_tc_persistent (tcgen05 kind::tf32, 3 passes, lo parts "
                                  "derived in shared memory)",
+                       "implicit_conv_ms": conv_ms,
+                       "implicit_conv_tflops": 2.0 * m * n * k / (conv_ms * 1e-3) / 1e12,
+                       "implicit_conv_note": "the forward of this layer as the step runs it "
+                                             "(sf_conv2d_tc: im2col rows gathered by the GEMM; "
+                                             "L2-bandwidth bound at N = 64)",
                        "shape_mnk": [m, n, k], "ms": ms, "bound": "tensor",
                        "achieved": useful, "unit": "TFLOP/s (useful fp32 MACs x2)",
                        "peak": peak, "frac": useful / peak,
