@@ -229,8 +229,9 @@ int sf_gemm_tf32x3_ex(int dev, int64_t m, int64_t n, int64_t k, int a_mn, int b_
                       const void* b_lo, void** c);
 /* Implicit-GEMM convolution on tcgen05 (3xTF32), NHWC float32:
  * out[n*ho*wo, co] = im2col(x) . W with W (kh*kw*c, co) row-major and
- * g8 = {N, H, W, C, KH, KW, stride, pad}; the im2col rows are gathered into
- * shared memory by the GEMM itself (never materialised).  Requires
+ * g8 = {N, H, W, C, KH, KW, stride, pad}; the im2col rows are loaded into
+ * shared memory by the GEMM itself (TMA im2col boxes, or cp.async gathers
+ * where the driver has no im2col maps) and never materialised.  Requires
  * C % 32 == 0 and co % 4 == 0 (else SF_ERR_INVALID).  Bit-identical to
  * sf_im2col + sf_gemm_tf32x3_ex.  Replaces the im2col + GEMM of the
  * reference's conv2d plugin kernel (oracle/ref_plugins.py, the numpy

@@ -243,6 +243,8 @@ int sf_init(int* n_devices) {
   SF_TRY(resolve("cuFuncSetAttribute", &drv.funcSetAttribute));
   SF_TRY(resolve("cuLaunchKernel", &drv.launchKernel));
   SF_TRY(resolve("cuTensorMapEncodeTiled", &drv.tensorMapEncodeTiled));
+  if (resolve("cuTensorMapEncodeIm2col", &drv.tensorMapEncodeIm2col) != SF_OK)
+    drv.tensorMapEncodeIm2col = nullptr;
   for (int i = 0; i < n && i < 64; ++i) {
     auto d = std::make_unique<Device>();
     d->id = i;

@@ -52,7 +52,8 @@ LO_IN_SMEM = True
 # float32 convolutions with C % 32 == 0 as implicit GEMMs (sf_conv2d_tc: no
 # materialised im2col matrix); bit-identical to the explicit path
 IMPLICIT_CONV = __import__("os").environ.get("SF_IMPLICIT_CONV", "1") == "1"
-IMPLICIT_MAX_K = int(__import__("os").environ.get("SF_IMPLICIT_MAX_K", "1152"))
+IMPLICIT_MAX_K = int(__import__("os").environ.get("SF_IMPLICIT_MAX_K", str(1 << 30)))
+IMPLICIT_STRIDED = __import__("os").environ.get("SF_IMPLICIT_STRIDED", "1") == "1"
 
 
 def _lo(pair) -> int:
@@ -117,13 +118,11 @@ def _conv_kernel(attrs, inputs, env):
     dev = ordinal_of(env.device)
     m, k = n * ho * wo, kh * kw * c
     if _use_tc(x.dtype) and IMPLICIT_CONV and c % 32 == 0 and co % 4 == 0 and \
-            not _is_pointwise(kh, kw, s, p) and s == 1 and k <= IMPLICIT_MAX_K:
-        # implicit GEMM: the im2col rows are gathered by the GEMM itself
-        # (B200, ResNet-50 b32 forward: layer1 3x3 167 -> 141 us, layer2
-        # 109 -> 92 us; slower where the 16-byte cp.async gathers of long
-        # contractions / strided windows replace one TMA box: layer3 80 ->
-        # 87 us, layer4 79 -> 103 us, 1x1 stride 2 54 -> 65 us —
-        # tools/conv_time.py)
+            not _is_pointwise(kh, kw, s, p) and (s == 1 or IMPLICIT_STRIDED) \
+            and k <= IMPLICIT_MAX_K:
+        # implicit GEMM: the GEMM loads its im2col rows itself (TMA im2col
+        # boxes; csrc/sf_gemm_tc.cu launch_conv_tc) — faster than im2col +
+        # GEMM at every ResNet-50 layer shape (tools/conv_time.py)
         out = _native.nn_call("sf_conv2d_tc", dev, _geom(n, h, wd, c, kh, kw, s, p), co,
                               x._ptr(), w._ptr(), out_nbytes=m * co * 4)
     elif _use_tc(x.dtype):
